@@ -1,0 +1,567 @@
+"""Overlap-save planner and convolution engines (reference: olsconv/ols.py).
+
+The planner and geometry are the reference's integer math, line for line in
+behaviour (ols.py:53-155), so plans and output windows are identical.  The
+engines run on the GPU:
+
+* ``fused`` — the product: one sm_100a kernel per call (C ABI
+  ``olsb_fused_c2c``) doing the paper's Algorithm 2 per segment: gather the
+  overlapped window, forward FFT in registers/shared memory, then per filter
+  multiply with the cached spectrum, inverse FFT and write the valid samples.
+* ``pipelined`` — the paper's cuFFT-OLS comparison point (Algorithm 1,
+  reference _pipelined ols.py:363-410): gather segments, batched cuFFT C2C,
+  a materialized (n_fil, rows, n) product, batched inverse cuFFT, discard.
+  Chunked over segments so the product tensor fits a memory budget.
+* ``full_fft_baseline`` — one padded cuFFT convolution of the whole signal.
+* ``direct_oracle`` — direct time-domain convolution on the GPU in float64
+  (the reference's ground-truth variant, oracle.py:20-41).
+
+Segments write disjoint output windows, so any split of the segment range
+(``workers`` launches, shards on several GPUs, host-streaming chunks) gives
+bit-identical results.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass
+from typing import Iterable, List, Optional, Tuple
+
+import numpy as np
+import torch
+
+from . import _lib
+from .core import FilterSet, Precision, Signal, make_filterset, make_signal
+from .errors import (BadLength, DomainMismatch, EngineError, FilterTooLong,
+                     HaloUnavailable, LayoutMismatch, PlanMismatch,
+                     SegmentTooSmall, TooLarge)
+from .fft import DEFAULT_MAX_FFT_LEN
+from .postproc import NONE, PostProcSpec
+
+MODES = ("c2c", "r2r")
+ENGINE_VARIANTS = ("fused", "pipelined", "full_fft_baseline", "direct_oracle")
+
+DEFAULT_MAX_FULL_LEN = 1 << 25
+PIPELINED_DEFAULT_SEGMENT = 8192
+# bytes of the materialized cuFFT-OLS product tensor per chunk
+PIPELINED_BUDGET_BYTES = 2 << 30
+
+
+@dataclass(frozen=True)
+class SegmentPlan:
+    """Blocking geometry (ols.py:53-66): segment s reads the zero-extended
+    input window [s*valid_len - (tap_len-1) + origin, ... + fft_len) and writes
+    output window [s*valid_len, min((s+1)*valid_len, signal_len))."""
+
+    fft_len: int
+    tap_len: int
+    valid_len: int
+    n_segments: int
+    signal_len: int
+    mode: str
+    origin: int
+
+
+def next_pow2(n: int) -> int:
+    return 1 if n <= 1 else 1 << (n - 1).bit_length()
+
+
+def _is_pow2(n: int) -> bool:
+    return n >= 1 and (n & (n - 1)) == 0
+
+
+def auto_segment_len(tap_len: int, variant: str = "fused",
+                     max_fft_len: int = DEFAULT_MAX_FFT_LEN) -> int:
+    """Untuned default segment length (ols.py:76-87)."""
+    if variant == "pipelined":
+        return max(PIPELINED_DEFAULT_SEGMENT, next_pow2(tap_len))
+    n = max(64, next_pow2(4 * (tap_len - 1)))
+    return min(n, max_fft_len)
+
+
+def plan(signal_len: int, tap_len: int, mode: str, origin: int = 0,
+         fft_len: Optional[int] = None,
+         max_fft_len: int = DEFAULT_MAX_FFT_LEN) -> SegmentPlan:
+    """Overlap-save geometry with the reference's validation order and
+    exceptions (ols.py:90-120)."""
+    if mode not in MODES:
+        raise ValueError(f"mode must be one of {MODES}, got {mode!r}")
+    if signal_len < 1 or tap_len < 1:
+        raise ValueError("signal and filter must be non-empty")
+    if not 0 <= origin <= tap_len - 1:
+        raise ValueError(f"origin {origin} outside [0, {tap_len - 1}]")
+    if tap_len > max_fft_len:
+        raise FilterTooLong(
+            f"tap length {tap_len} exceeds max segment length {max_fft_len};"
+            " use full_fft_convolve")
+    if fft_len is None or fft_len == "auto":
+        n = auto_segment_len(tap_len, max_fft_len=max_fft_len)
+    else:
+        n = int(fft_len)
+        floor = 8 if mode == "r2r" else 4
+        if not _is_pow2(n) or n < floor:
+            raise BadLength(
+                f"segment length must be a power of two >= {floor}, got {n}")
+        if n < tap_len:
+            raise SegmentTooSmall(
+                f"segment length {n} shorter than filter ({tap_len} taps)")
+    valid = n - tap_len + 1
+    n_seg = -(-signal_len // valid)
+    return SegmentPlan(fft_len=n, tap_len=tap_len, valid_len=valid,
+                       n_segments=n_seg, signal_len=signal_len, mode=mode,
+                       origin=origin)
+
+
+def _geometry(seg_plan: SegmentPlan, halo: int) -> Tuple[int, int, int, int]:
+    """(l_eff, t0, win_off, n_seg_eff) for a post-processing halo
+    (ols.py:123-146)."""
+    m = seg_plan.tap_len
+    o = seg_plan.origin
+    if halo == 0 or m == 1:
+        l_eff = seg_plan.valid_len
+        t0 = m - 1
+        win_off = o - (m - 1)
+    else:
+        l_eff = seg_plan.valid_len - 2 * halo
+        t0 = m - 1 + halo
+        win_off = o - (m - 1) - halo
+        if l_eff < 1:
+            raise HaloUnavailable(
+                f"segment length {seg_plan.fft_len} leaves no room for a"
+                f" halo of {halo} around {seg_plan.tap_len} taps")
+    n_seg_eff = -(-seg_plan.signal_len // l_eff)
+    return l_eff, t0, win_off, n_seg_eff
+
+
+def output_windows(seg_plan: SegmentPlan,
+                   postproc: PostProcSpec = NONE) -> List[Tuple[int, int]]:
+    """Per-segment output windows: disjoint, covering [0, signal_len)
+    (ols.py:149-155)."""
+    l_eff, _, _, n_seg = _geometry(seg_plan, postproc.halo)
+    n_s = seg_plan.signal_len
+    return [(s * l_eff, min((s + 1) * l_eff, n_s)) for s in range(n_seg)]
+
+
+def _chunk_bounds(n_items: int, workers: int) -> List[Tuple[int, int]]:
+    """Contiguous item ranges (ols.py:212-215); also the multi-GPU shard map."""
+    k = max(1, min(workers, n_items))
+    step = -(-n_items // k)
+    return [(lo, min(lo + step, n_items)) for lo in range(0, n_items, step)]
+
+
+def _required_layout(mode: str, variant: str) -> str:
+    return "permuted" if (mode == "c2c" and variant == "fused") else "natural"
+
+
+def _stream_ptr() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+# ---------------------------------------------------------------------------
+# filter spectra
+# ---------------------------------------------------------------------------
+
+def transform_filters(filters: FilterSet, seg_plan: SegmentPlan,
+                      layout: str = "natural") -> FilterSet:
+    """Zero-pad every filter to the segment length and cache its forward
+    transform (ols.py:168-205).  "permuted" spectra come from the engine's own
+    in-register FFT (olsb_filter_spectra_c2c), which also writes the coalesced
+    engine layout the fused kernel streams."""
+    if layout not in ("natural", "permuted"):
+        raise ValueError(f"layout must be natural|permuted, got {layout!r}")
+    if filters.tap_length != seg_plan.tap_len:
+        raise PlanMismatch(
+            f"filter tap length {filters.tap_length} != plan "
+            f"{seg_plan.tap_len}")
+    precision = (Precision.single
+                 if filters.taps.dtype in (torch.float32, torch.complex64)
+                 else Precision.double)
+    n = seg_plan.fft_len
+    taps = filters.taps
+    if seg_plan.mode == "r2r":
+        if filters.value_kind != "real":
+            raise PlanMismatch("complex filter taps on the real path")
+        if layout != "natural":
+            raise LayoutMismatch("packed real spectra are natural-order only")
+        padded = torch.zeros((filters.n_filters, n), dtype=precision.torch_real,
+                             device=taps.device)
+        padded[:, :filters.tap_length] = taps
+        spectra = torch.fft.rfft(padded, dim=1)
+        return filters.with_spectra(spectra, layout, n)
+    ctaps = taps.to(precision.torch_complex).contiguous()
+    if layout == "permuted":
+        spectra = torch.empty((filters.n_filters, n),
+                              dtype=precision.torch_complex, device=taps.device)
+        dev = torch.empty_like(spectra)
+        with torch.cuda.device(taps.device):
+            _lib.call("olsb_filter_spectra_c2c", ctaps.data_ptr(),
+                      filters.n_filters, filters.tap_length, n,
+                      spectra.data_ptr(), dev.data_ptr(), precision.code,
+                      _stream_ptr())
+        return filters.with_spectra(spectra, layout, n, dev)
+    padded = torch.zeros((filters.n_filters, n), dtype=precision.torch_complex,
+                         device=taps.device)
+    padded[:, :filters.tap_length] = ctaps
+    return filters.with_spectra(torch.fft.fft(padded, dim=1), layout, n)
+
+
+def _engine_spectra(filters: FilterSet) -> torch.Tensor:
+    """Engine-layout spectra; converted once from a permuted cache that was
+    filled elsewhere (e.g. handed over from the reference)."""
+    if filters.spectra_dev is not None:
+        return filters.spectra_dev
+    spec = filters.spectra.contiguous()
+    dev = torch.empty_like(spec)
+    prec = Precision.single if spec.dtype == torch.complex64 else Precision.double
+    _lib.call("olsb_spectra_perm_to_dev", spec.data_ptr(), spec.shape[0],
+              spec.shape[1], dev.data_ptr(), prec.code, _stream_ptr())
+    object.__setattr__(filters, "spectra_dev", dev)
+    return dev
+
+
+# ---------------------------------------------------------------------------
+# engines
+# ---------------------------------------------------------------------------
+
+def _check_inputs(signal: Signal, filters: FilterSet, seg_plan: SegmentPlan):
+    """Validation in the reference's order (ols.py:232-254)."""
+    if signal.domain != "time":
+        raise DomainMismatch("convolution needs a time-domain signal")
+    if signal.length != seg_plan.signal_len:
+        raise PlanMismatch(
+            f"signal length {signal.length} != plan {seg_plan.signal_len}")
+    if filters.tap_length != seg_plan.tap_len:
+        raise PlanMismatch(
+            f"filter tap length {filters.tap_length} != plan "
+            f"{seg_plan.tap_len}")
+    if filters.origin != seg_plan.origin:
+        raise PlanMismatch(
+            f"filter origin {filters.origin} != plan {seg_plan.origin}")
+    if seg_plan.mode == "r2r":
+        if signal.value_kind != "real" or filters.value_kind != "real":
+            raise PlanMismatch("r2r mode needs real signal and filters")
+    else:
+        if signal.value_kind != "complex":
+            raise PlanMismatch("c2c mode needs a complex signal")
+    sig_single = signal.samples.dtype in (torch.float32, torch.complex64)
+    fil_single = filters.taps.dtype in (torch.float32, torch.complex64)
+    if sig_single != fil_single:
+        raise PlanMismatch("signal and filters must share one precision")
+
+
+def convolve(signal: Signal, filters: FilterSet, seg_plan: SegmentPlan,
+             variant: str = "fused", postproc: Optional[PostProcSpec] = None,
+             workers: int = 1, out: Optional[torch.Tensor] = None,
+             chunk_segments: Optional[int] = None) -> torch.Tensor:
+    """Convolve the signal with every filter; returns (n_fil, signal_len)
+    (ols.py:257-316).
+
+    Extensions over the reference (all optional):
+      out             preallocated result (CUDA, or pinned CPU memory: then
+                      the fused engine streams segment chunks host->device->
+                      host with copies overlapped with compute);
+      chunk_segments  segments per streaming chunk (host path).
+    ``workers`` splits the segment range into that many launches; results
+    are bit-identical for any value (test_ols.py:242-251).
+    """
+    pp = postproc if postproc is not None else NONE
+    if variant not in ENGINE_VARIANTS:
+        raise ValueError(f"variant must be one of {ENGINE_VARIANTS}")
+    _check_inputs(signal, filters, seg_plan)
+    precision = signal.precision
+
+    if variant == "direct_oracle":
+        return _direct(signal, filters, pp)
+    if variant == "full_fft_baseline":
+        return full_fft_convolve(signal, filters, pp)
+
+    layout = _required_layout(seg_plan.mode, variant)
+    if filters.spectra is None:
+        filters = transform_filters(filters, seg_plan, layout)
+    else:
+        if filters.spectra_n != seg_plan.fft_len:
+            raise PlanMismatch(
+                f"cached spectra built for length {filters.spectra_n},"
+                f" plan wants {seg_plan.fft_len}")
+        if filters.spectra_layout != layout:
+            raise LayoutMismatch(
+                f"cached spectra layout {filters.spectra_layout!r} does not"
+                f" match the {variant} engine's transform ({layout!r})")
+        want_bins = (seg_plan.fft_len // 2 + 1 if seg_plan.mode == "r2r"
+                     else seg_plan.fft_len)
+        if filters.spectra.shape[1] != want_bins:
+            raise PlanMismatch("cached spectra do not match the plan's mode")
+
+    n_s = signal.length
+    n_fil = filters.n_filters
+    real_out = seg_plan.mode == "r2r" or pp.real_output
+    out_dtype = precision.torch_real if real_out else precision.torch_complex
+
+    if pp.kind == "derivative" and n_s == 1:
+        return torch.zeros((n_fil, 1), dtype=out_dtype,
+                           device=signal.samples.device)
+
+    l_eff, t0, win_off, n_seg_eff = _geometry(seg_plan, pp.halo)
+    if seg_plan.mode == "r2r" or pp.kind not in ("none", "scale"):
+        raise EngineError(
+            f"mode {seg_plan.mode!r} with postproc {pp.kind!r} is not in this "
+            "build's fused engine (SURVEY §8(f) rows 2-3)")
+    if out is not None:
+        if tuple(out.shape) != (n_fil, n_s) or out.dtype != out_dtype:
+            raise ValueError(f"out must be {(n_fil, n_s)} {out_dtype}")
+        if not out.is_contiguous():
+            raise ValueError("out must be contiguous")
+
+    if variant == "fused":
+        spec_dev = _engine_spectra(filters)
+        if out is not None and not out.is_cuda:
+            return _fused_streaming(signal, spec_dev, seg_plan, pp, precision,
+                                    l_eff, t0, win_off, n_seg_eff, out,
+                                    chunk_segments)
+        if not signal.samples.is_cuda:
+            raise ValueError("a host-resident signal needs a host `out` "
+                             "(streaming path)")
+        if out is None:
+            out = torch.empty((n_fil, n_s), dtype=out_dtype,
+                              device=signal.samples.device)
+        with torch.cuda.device(signal.samples.device):
+            for lo, hi in _chunk_bounds(n_seg_eff, workers):
+                fused_launch(signal.samples, 0, n_s, spec_dev, n_fil, seg_plan,
+                             l_eff, t0, win_off, lo, hi, pp, out, n_s, 0,
+                             precision)
+        return out
+    return _pipelined(signal, filters, seg_plan, pp, precision, l_eff, t0,
+                      win_off, n_seg_eff, out)
+
+
+def fused_launch(x: torch.Tensor, x_base: int, n_s: int,
+                 spec_dev: torch.Tensor, n_fil: int, seg_plan: SegmentPlan,
+                 l_eff: int, t0: int, win_off: int, seg_lo: int, seg_hi: int,
+                 pp: PostProcSpec, out: torch.Tensor, out_ld: int,
+                 out_base: int, precision: Precision,
+                 stream: Optional[int] = None) -> None:
+    """One call of the C-ABI fused kernel (the reference's K.fused_c2c,
+    _kernels_nb.py:265-285) on the current stream."""
+    _lib.call("olsb_fused_c2c", x.data_ptr(), x_base, n_s, spec_dev.data_ptr(),
+              n_fil, seg_plan.fft_len, seg_plan.tap_len, seg_plan.origin,
+              l_eff, t0, win_off, seg_lo, seg_hi, pp.code, float(pp.scale),
+              out.data_ptr(), out_ld, out_base, precision.code,
+              _stream_ptr() if stream is None else stream)
+
+
+def _fused_streaming(signal, spec_dev, seg_plan, pp, precision, l_eff, t0,
+                     win_off, n_seg, out, chunk_segments):
+    """Host-memory path: per chunk of segments, H2D of its input window,
+    fused kernel into a device staging tile, strided D2H into ``out``.
+    Three streams rotate over three staging slots so copies in both
+    directions overlap the kernel of the neighbouring chunks."""
+    n = seg_plan.fft_len
+    n_s = signal.length
+    n_fil = spec_dev.shape[0]
+    x_host = signal.samples
+    dev = spec_dev.device
+    esize = out.element_size()
+    if chunk_segments is None:
+        # ~256 MiB of output per chunk
+        chunk_segments = max(1, (256 << 20) // max(1, n_fil * l_eff * esize))
+    chunks = [(lo, min(lo + chunk_segments, n_seg))
+              for lo in range(0, n_seg, chunk_segments)]
+    nslot = min(3, len(chunks))
+    w_max = chunk_segments * l_eff
+    x_len_max = w_max + n
+    with torch.cuda.device(dev):
+        streams = [torch.cuda.Stream() for _ in range(nslot)]
+        xbuf = [torch.empty(x_len_max, dtype=x_host.dtype, device=dev)
+                for _ in range(nslot)]
+        obuf = [torch.empty((n_fil, w_max), dtype=out.dtype, device=dev)
+                for _ in range(nslot)]
+        ready = torch.cuda.current_stream()
+        for s in streams:
+            s.wait_stream(ready)
+        lib = _lib.load()
+        for i, (lo, hi) in enumerate(chunks):
+            k = i % nslot
+            st = streams[k]
+            g_lo = lo * l_eff
+            g_hi = min(hi * l_eff, n_s)
+            xa = max(0, g_lo + win_off)
+            xb = min(n_s, (hi - 1) * l_eff + win_off + n)
+            with torch.cuda.stream(st):
+                if xb > xa:
+                    xbuf[k][:xb - xa].copy_(x_host[xa:xb], non_blocking=True)
+                fused_launch(xbuf[k], xa, n_s, spec_dev, n_fil, seg_plan,
+                             l_eff, t0, win_off, lo, hi, pp, obuf[k], w_max,
+                             g_lo, precision, st.cuda_stream)
+                _lib.check(lib.olsb_copy2d_async(
+                    out.data_ptr() + g_lo * esize, n_s * esize,
+                    obuf[k].data_ptr(), w_max * esize, (g_hi - g_lo) * esize,
+                    n_fil, 0, st.cuda_stream), "olsb_copy2d_async")
+        for s in streams:
+            ready.wait_stream(s)
+        # keep the staging buffers alive until the copies retire
+        for s in streams:
+            s.synchronize()
+    return out
+
+
+def _pipelined(signal, filters, seg_plan, pp, precision, l_eff, t0, win_off,
+               n_seg, out):
+    """cuFFT-based OLS, the paper's comparison point (Algorithm 1;
+    reference _pipelined ols.py:363-410): gather -> batched C2C forward ->
+    materialized product -> batched C2C inverse -> discard + store.  Chunked
+    so the (n_fil, rows, n) product stays within PIPELINED_BUDGET_BYTES."""
+    n = seg_plan.fft_len
+    n_s = signal.length
+    x = signal.samples
+    spectra = filters.spectra  # natural order
+    n_fil = filters.n_filters
+    dev = x.device
+    if out is None:
+        out = torch.empty((n_fil, n_s), dtype=precision.torch_complex,
+                          device=dev)
+    esize = out.element_size()
+    rows_per = max(1, PIPELINED_BUDGET_BYTES // (2 * n_fil * n * esize))
+    ar = torch.arange(n, device=dev)
+    for lo in range(0, n_seg, rows_per):
+        hi = min(lo + rows_per, n_seg)
+        starts = torch.arange(lo, hi, device=dev) * l_eff + win_off
+        idx = starts[:, None] + ar[None, :]
+        ok = (idx >= 0) & (idx < n_s)
+        mat = torch.where(ok, x[idx.clamp(0, n_s - 1)],
+                          torch.zeros((), dtype=x.dtype, device=dev))
+        fmat = torch.fft.fft(mat, dim=1)
+        mid = torch.fft.ifft(fmat[None, :, :] * spectra[:, None, :], dim=2)
+        valid = mid[:, :, t0:t0 + l_eff].reshape(n_fil, -1)
+        g_lo = lo * l_eff
+        g_hi = min(hi * l_eff, n_s)
+        seg_out = valid[:, :g_hi - g_lo]
+        if pp.kind == "scale":
+            seg_out = seg_out * pp.scale
+        out[:, g_lo:g_hi] = seg_out
+    return out
+
+
+def _direct(signal: Signal, filters: FilterSet, pp: PostProcSpec):
+    """Direct time-domain convolution on the GPU, float64 accumulate, rounded
+    to the signal's precision (oracle.py:20-41): y[f,n] = sum_k h[f,k]
+    x[n-k+o], zeros off the ends.  Complex conv = 4 real conv1d calls."""
+    if pp.kind not in ("none", "scale"):
+        raise EngineError("direct_oracle supports postproc none|scale only")
+    x = signal.samples.to(torch.complex128)
+    h = filters.taps.to(torch.complex128)
+    m = filters.tap_length
+    o = filters.origin
+    n_s = signal.length
+    # cross-correlation with flipped taps == convolution
+    hf = torch.flip(h, dims=[1])
+    pad_l, pad_r = m - 1 - o, o
+    xr = torch.nn.functional.pad(x.real[None, None], (pad_l, pad_r))
+    xi = torch.nn.functional.pad(x.imag[None, None], (pad_l, pad_r))
+    wr = hf.real[:, None, :].contiguous()
+    wi = hf.imag[:, None, :].contiguous()
+    conv = torch.nn.functional.conv1d
+    yr = conv(xr, wr)[0] - conv(xi, wi)[0]
+    yi = conv(xr, wi)[0] + conv(xi, wr)[0]
+    y = torch.complex(yr, yi)[:, :n_s]
+    if pp.kind == "scale":
+        y = y * pp.scale
+    return y.to(signal.precision.torch_complex)
+
+
+def full_fft_convolve(signal: Signal, filters: FilterSet,
+                      postproc: Optional[PostProcSpec] = None,
+                      max_len: int = DEFAULT_MAX_FULL_LEN) -> torch.Tensor:
+    """No-segmentation baseline (ols.py:413-464): one cuFFT convolution of the
+    whole signal padded to next_pow2(n_s + m - 1)."""
+    pp = postproc if postproc is not None else NONE
+    if signal.domain != "time":
+        raise DomainMismatch("convolution needs a time-domain signal")
+    if signal.value_kind == "real" and filters.value_kind == "complex":
+        raise PlanMismatch("complex filter taps on a real signal")
+    if pp.kind not in ("none", "scale"):
+        raise EngineError("full_fft_convolve supports postproc none|scale only")
+    precision = signal.precision
+    n_s = signal.length
+    m = filters.tap_length
+    o = filters.origin
+    real_path = signal.value_kind == "real"
+    padded_len = max(8 if real_path else 4, next_pow2(n_s + m - 1))
+    if padded_len > max_len:
+        raise TooLarge(
+            f"padded length {padded_len} exceeds the {max_len}-sample budget")
+    x = signal.samples
+    h = filters.taps
+    if real_path:
+        full = torch.fft.irfft(torch.fft.rfft(x, n=padded_len)[None, :]
+                               * torch.fft.rfft(h, n=padded_len, dim=1),
+                               n=padded_len, dim=1)
+    else:
+        h = h.to(precision.torch_complex)
+        full = torch.fft.ifft(torch.fft.fft(x, n=padded_len)[None, :]
+                              * torch.fft.fft(h, n=padded_len, dim=1), dim=1)
+    y = full[:, o:o + n_s]
+    if pp.kind == "scale":
+        y = y * pp.scale
+    return y.contiguous()
+
+
+# ---------------------------------------------------------------------------
+# segment-size autotuning (ols.py:471-526), timed with CUDA events
+# ---------------------------------------------------------------------------
+
+def measure_segment_times(tap_len: int, mode: str, candidates: Iterable[int],
+                          probe_len: int = 1 << 18, n_filters: int = 4,
+                          repeats: int = 3,
+                          precision: Precision = Precision.single,
+                          seed: int = 0) -> dict:
+    """Median fused-engine device time per feasible candidate length."""
+    floor = 8 if mode == "r2r" else 4
+    feasible = sorted(c for c in set(candidates)
+                      if _is_pow2(c) and c >= max(tap_len, floor))
+    if not feasible:
+        raise SegmentTooSmall(
+            f"no candidate segment length fits {tap_len} taps")
+    if mode != "c2c":
+        raise EngineError("the fused engine of this build is c2c only")
+    rng = np.random.default_rng(seed)
+    sig = make_signal(rng.standard_normal(probe_len)
+                      + 1j * rng.standard_normal(probe_len), "complex",
+                      precision)
+    taps = (rng.standard_normal((n_filters, tap_len))
+            + 1j * rng.standard_normal((n_filters, tap_len)))
+    fs = make_filterset(taps, 0, precision)
+    times = {}
+    for cand in feasible:
+        p = plan(probe_len, tap_len, mode, 0, cand,
+                 max_fft_len=max(cand, DEFAULT_MAX_FFT_LEN))
+        if cand > DEFAULT_MAX_FFT_LEN:
+            continue
+        cached = transform_filters(fs, p, _required_layout(mode, "fused"))
+        out = convolve(sig, cached, p)
+        samples = []
+        for _ in range(repeats):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            convolve(sig, cached, p, out=out)
+            e1.record()
+            e1.synchronize()
+            samples.append(e0.elapsed_time(e1) * 1e-3)
+        times[cand] = float(np.median(samples))
+    return times
+
+
+def autotune_segment_size(tap_len: int, mode: str,
+                          candidates: Optional[Iterable[int]] = None,
+                          probe_len: int = 1 << 18, **kwargs) -> int:
+    """Fastest candidate; ties go to the smaller length (ols.py:511-526)."""
+    if candidates is None:
+        candidates = [1 << b for b in range(6, 13)]
+    times = measure_segment_times(tap_len, mode, candidates, probe_len,
+                                  **kwargs)
+    best_n, best_t = None, math.inf
+    for cand in sorted(times):
+        if times[cand] < best_t:
+            best_n, best_t = cand, times[cand]
+    return best_n
