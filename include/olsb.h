@@ -98,6 +98,25 @@ int olsb_fused_c2c(const void* x, int64_t x_base, int64_t n_s,
                    void* out, int64_t out_ld, int64_t out_base,
                    int precision, void* stream);
 
+/* Output-range form of olsb_fused_c2c for sharded and streamed signals
+ * (no reference counterpart): writes outputs [g_lo, g_hi) of every filter
+ * for the plain (no post-processing halo) geometry of taps of length m with
+ * output origin `origin`.  The engine covers the range with its own segment
+ * grid, anchored at global sample 0, so results are bit-identical for any
+ * partition of [0, n_s) into ranges.  `x`, `x_base`, `n_s`, `out`, `out_ld`,
+ * `out_base` as in olsb_fused_c2c; the input samples a call reads are
+ * [x_lo, x_hi) of olsb_input_extent (clipped to [0, n_s)). */
+int olsb_fused_c2c_range(const void* x, int64_t x_base, int64_t n_s,
+                         const void* spectra_dev, int n_fil, int n, int m,
+                         int origin, int64_t g_lo, int64_t g_hi, int pp_kind,
+                         double pp_c, void* out, int64_t out_ld,
+                         int64_t out_base, int precision, void* stream);
+
+/* Input samples [*x_lo, *x_hi) that olsb_fused_c2c_range(g_lo, g_hi) reads
+ * (before clipping to [0, n_s)): the shard plus its halos. */
+int olsb_input_extent(int n, int m, int origin, int64_t g_lo, int64_t g_hi,
+                      int64_t* x_lo, int64_t* x_hi);
+
 /* Tuning knob (not in the reference): number of filters processed per work
  * item (0 = all).  Smaller chunks cut the tail of the last wave at the cost
  * of recomputing the segment's forward FFT per chunk. */

@@ -1,0 +1,725 @@
+// olsb_engine.cuh — sm_100a kernels of the OLS engine (device code).
+//
+//   fused_c2c_kernel  the hot path: segment staging -> forward FFT -> per
+//                     filter {multiply, inverse FFT, valid-sample writeback}
+//                     (reference: _kernels_nb.py:265-285, ols.py:319-360)
+//   fwd_rows_kernel   forward transform of rows (filter spectra,
+//                     fft_forward_permuted); same passes as the fused kernel
+//   inv_rows_kernel   inverse transform of rows (fft_inverse_permuted)
+//   perm_to_dev_kernel  reference permuted layout -> engine layout
+//
+// One thread owns E = 16 samples of a segment; T = N / 16 threads form a
+// segment group and SEGS groups a CTA.  Samples move between 4-bit windows
+// through padded, bank-conflict-free shared memory (olsb_fft.cuh).  The
+// segment spectrum stays in registers for the whole filter loop; the kernel
+// shape (groups per CTA, exchange buffers, how filter spectra are staged,
+// barrier scope) is a compile-time policy, tuned per N (olsb_kernels.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "olsb.h"
+#include "olsb_fft.cuh"
+
+namespace olsb {
+
+// 16-byte vector type holding two complex<float> or one complex<double>
+template <class R>
+struct V16;
+template <>
+struct V16<float> {
+  using type = float4;
+  static constexpr int per = 2;  // complex per vector
+};
+template <>
+struct V16<double> {
+  using type = double2;
+  static constexpr int per = 1;
+};
+
+// How the fused kernel stages filter spectra:
+enum HMode : int {
+  H_LDG = 0,    // read through L1 with __ldg at the multiply
+  H_TMA = 1,    // CTA-shared double buffer filled by TMA bulk copies
+  H_ASYNC = 2,  // per-thread cp.async prefetch of the next filter's values
+  H_TEX = 3,    // texture fetches: the TEX data path runs beside the LSU
+                // pipe that carries the shared-memory exchanges
+};
+
+// Kernel configuration.  SEGS segment groups per CTA, NBUF exchange buffers
+// per group (2: one barrier per exchange, 1: two), HM spectrum staging, BAR
+// barrier scope (0: CTA-wide __syncthreads, 1: named barrier per group),
+// MINB target CTAs per SM (register cap).
+template <class R_, int LOGN_, int SEGS_, int NBUF_, int HM_, int BAR_,
+          int MINB_>
+struct KCfg {
+  using R = R_;
+  static constexpr int LOGN = LOGN_;
+  using G = Geo<LOGN>;
+  using L = SmemLayout<R, LOGN>;
+  static constexpr bool dbl = std::is_same<R, double>::value;
+  static constexpr int E = G::E, T = G::T, P = G::P, LOGE = G::LOGE;
+  static constexpr int SEGS = SEGS_;
+  static constexpr int THREADS = SEGS * T;
+  static constexpr int NBUF = NBUF_;
+  static constexpr int HM = HM_;
+  static constexpr int BAR = (BAR_ && T >= 32 && SEGS > 1) ? 1 : 0;
+  static constexpr int MINB = MINB_;
+  static constexpr int VPT = E / V16<R>::per;  // 16-B vectors per thread (J)
+  // top-window twiddles live in registers (float: 30 registers) and its
+  // table is built inside the exchange buffers, which it only occupies until
+  // the registers are loaded
+  static constexpr bool TOPREG = !dbl && P >= 2;
+  static constexpr size_t al(size_t b) { return (b + 127) & ~size_t(127); }
+  static constexpr size_t buf_elems = size_t(SEGS) * L::stride;
+  static constexpr size_t bufs_bytes =
+      P >= 2 ? al(NBUF * buf_elems * sizeof(Cpx<R>)) : 0;
+  // ---- row kernels: every twiddle table in shared memory, then buffers
+  static constexpr size_t tab_bytes = al(size_t(G::tw_total()) * sizeof(Tw<R>));
+  static constexpr size_t smem_bytes = tab_bytes + bufs_bytes;
+  // ---- fused kernel: [bufs (+ top table at init) | low tables | H | bars]
+  static constexpr int lowtab_elems = TOPREG ? G::tw_offset(P - 1) : G::tw_total();
+  static constexpr size_t f_bufs_bytes =
+      P >= 2 ? std::max(bufs_bytes,
+                        TOPREG ? al(size_t(G::tw_entries(P - 1)) * sizeof(Tw<R>))
+                               : size_t(0))
+             : 0;
+  static constexpr size_t f_tab_off = f_bufs_bytes;
+  static constexpr size_t f_tab_bytes = al(size_t(lowtab_elems) * sizeof(Tw<R>));
+  static constexpr size_t f_h_off = f_tab_off + f_tab_bytes;
+  static constexpr size_t h_bytes = size_t(G::N) * sizeof(Cpx<R>);
+  static constexpr size_t f_h_bytes =
+      HM == H_TMA ? 2 * h_bytes
+                  : (HM == H_ASYNC ? al(size_t(THREADS) * VPT * 16) : 0);
+  static constexpr size_t f_bar_off = f_h_off + f_h_bytes;
+  static constexpr size_t f_smem_bytes = f_bar_off + 16;
+};
+
+// configuration of the row kernels (filter spectra, standalone transforms)
+template <class R, int LOGN>
+using RowCfg = KCfg<R, LOGN,
+                    std::max(1, ((!std::is_same<R, double>::value && LOGN == 12)
+                                     ? 512 : 256) >> Geo<LOGN>::LOGT),
+                    std::is_same<R, double>::value ? 1 : 2, H_LDG, 0, 1>;
+
+// ---------------------------------------------------------------------------
+// barriers
+// ---------------------------------------------------------------------------
+template <class C>
+__device__ __forceinline__ void group_sync(int sl) {
+  if constexpr (C::BAR == 1) {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + sl), "r"(C::T) : "memory");
+  } else {
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// shared-memory window I/O (addresses = per-thread base + immediates)
+// ---------------------------------------------------------------------------
+template <class C, int Q>
+__device__ __forceinline__ void smem_store(Cpx<typename C::R>* __restrict__ seg_buf,
+                                           int t, const Cpx<typename C::R>* x) {
+  using R = typename C::R;
+  using G = typename C::G;
+  using L = typename C::L;
+  Cpx<R>* b = seg_buf + L::pos(G::thread_part(Q, t));
+  if constexpr (Q == 0 && !C::dbl && C::E >= 2) {
+    sfor<0, C::E / 2>([&](auto ec) {
+      constexpr int e = 2 * decltype(ec)::value;
+      constexpr int off = L::pos(G::elem_part(Q, e));
+      *reinterpret_cast<float4*>(b + off) =
+          make_float4(x[e].re, x[e].im, x[e + 1].re, x[e + 1].im);
+    });
+  } else {
+    sfor<0, C::E>([&](auto ec) {
+      constexpr int e = decltype(ec)::value;
+      constexpr int off = L::pos(G::elem_part(Q, e));
+      b[off] = x[e];
+    });
+  }
+}
+
+template <class C, int Q>
+__device__ __forceinline__ void smem_load(const Cpx<typename C::R>* __restrict__ seg_buf,
+                                          int t, Cpx<typename C::R>* x) {
+  using R = typename C::R;
+  using G = typename C::G;
+  using L = typename C::L;
+  const Cpx<R>* b = seg_buf + L::pos(G::thread_part(Q, t));
+  if constexpr (Q == 0 && !C::dbl && C::E >= 2) {
+    sfor<0, C::E / 2>([&](auto ec) {
+      constexpr int e = 2 * decltype(ec)::value;
+      constexpr int off = L::pos(G::elem_part(Q, e));
+      const float4 v = *reinterpret_cast<const float4*>(b + off);
+      x[e] = Cpx<R>{v.x, v.y};
+      x[e + 1] = Cpx<R>{v.z, v.w};
+    });
+  } else {
+    sfor<0, C::E>([&](auto ec) {
+      constexpr int e = decltype(ec)::value;
+      constexpr int off = L::pos(G::elem_part(Q, e));
+      x[e] = b[off];
+    });
+  }
+}
+
+// twiddle tables for windows 1..P-1 (double-precision math, rounded once).
+// Window q's table goes to lowtab + tw_offset(q), except the top window's
+// when `toptab` is given.
+template <class R, int LOGN>
+__device__ void build_tables(Tw<R>* lowtab, Tw<R>* toptab) {
+  using G = Geo<LOGN>;
+  sfor<1, G::P>([&](auto qc) {
+    constexpr int q = decltype(qc)::value;
+    constexpr int lo = G::lo(q);
+    constexpr int cnt = G::tw_entries(q);
+    Tw<R>* dst = (q == G::P - 1 && toptab) ? toptab : lowtab + G::tw_offset(q);
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+      int idx, l;
+      twiddle_decode(lo, i, &idx, &l);
+      double c, t;
+      twiddle_entry(lo, idx, l, G::tan01(q), &c, &t);
+      dst[i] = Tw<R>{R(c), R(t)};
+    }
+  });
+}
+
+// ---- TMA bulk copy + mbarrier, cp.async
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// one elected thread: global -> shared bulk copy completing on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src,
+                                        uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "r"(bytes)
+      : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "OLSB_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra OLSB_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+// predicated streaming store of one complex sample: stores iff o < span
+// (unsigned compare folds the o >= 0 test)
+__device__ __forceinline__ void st_cs_if(Cpx<float>* p, Cpx<float> v,
+                                         unsigned o, unsigned span) {
+  asm volatile(
+      "{\n .reg .pred q;\n setp.lt.u32 q, %3, %4;\n"
+      " @q st.global.cs.v2.f32 [%0], {%1, %2};\n}" ::"l"(p),
+      "f"(v.re), "f"(v.im), "r"(o), "r"(span)
+      : "memory");
+}
+__device__ __forceinline__ void st_cs_if(Cpx<double>* p, Cpx<double> v,
+                                         unsigned o, unsigned span) {
+  asm volatile(
+      "{\n .reg .pred q;\n setp.lt.u32 q, %3, %4;\n"
+      " @q st.global.cs.v2.f64 [%0], {%1, %2};\n}" ::"l"(p),
+      "d"(v.re), "d"(v.im), "r"(o), "r"(span)
+      : "memory");
+}
+
+// accessors of the thread's 15 runtime twiddles of window q (see
+// dit_pass_rt): a shared-memory table read with 128-bit pair loads, or
+// registers
+template <class R>
+struct TwSmem {
+  const Tw<R>* base;  // window table + 2 l
+  int lo;
+  __device__ __forceinline__ Tw<R> get0() const { return base[0]; }
+  __device__ __forceinline__ TwPair<R> get2(int p) const {
+    return *reinterpret_cast<const TwPair<R>*>(base + (size_t(p) << (lo + 1)));
+  }
+};
+template <class R>
+struct TwRegs {
+  const Tw<R>* r;  // indexed by idx
+  __device__ __forceinline__ Tw<R> get0() const { return r[0]; }
+  __device__ __forceinline__ TwPair<R> get2(int p) const {
+    return TwPair<R>{r[2 * p - 1], r[2 * p]};
+  }
+};
+
+template <class R, int LOGN, int Q>
+__device__ __forceinline__ TwSmem<R> tw_smem(const Tw<R>* tab, int t) {
+  using G = Geo<LOGN>;
+  return TwSmem<R>{tab + 2 * G::low_bits(Q, t), G::lo(Q)};
+}
+template <int LOGN, int Q>
+__device__ __forceinline__ int top_bits(int t) {
+  using G = Geo<LOGN>;
+  return G::lo(Q) >= 2 ? (G::low_bits(Q, t) >> (G::lo(Q) - 2)) & 3 : 0;
+}
+
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+// exchange: write window QW, barrier, read window QR.  `pre_bar` runs after
+// the stores, right before the barrier (used to fold a producer wait into it)
+template <class C, int QW, int QR, class H = NoHook, class H2 = NoHook>
+__device__ __forceinline__ void exchange(Cpx<typename C::R>* bufs, int& xc,
+                                         int sl, int t, Cpx<typename C::R>* x,
+                                         const H& pre_bar = H{},
+                                         const H2& post_bar = H2{}) {
+  Cpx<typename C::R>* buf = bufs + (C::NBUF == 2 ? (xc & 1) * C::buf_elems : 0) +
+                            size_t(sl) * C::L::stride;
+  if constexpr (C::NBUF == 1) group_sync<C>(sl);
+  smem_store<C, QW>(buf, t, x);
+  pre_bar();
+  group_sync<C>(sl);
+  post_bar();
+  smem_load<C, QR>(buf, t, x);
+  ++xc;
+}
+
+// full forward transform: x holds window P-1 on entry, window 0 (J) on exit.
+// With TOPREG the top window's 15 twiddles come from `twr`.
+template <class C, bool TOPREG, class H = NoHook, class H2 = NoHook>
+__device__ __forceinline__ void forward_fft(Cpx<typename C::R>* x,
+                                            const Tw<typename C::R>* lowtab,
+                                            const Tw<typename C::R>* twr,
+                                            Cpx<typename C::R>* bufs, int& xc,
+                                            int sl, int t,
+                                            const H& last_hook = H{},
+                                            const H2& post_hook = H2{}) {
+  using R = typename C::R;
+  using G = typename C::G;
+  constexpr int LOGN = C::LOGN;
+  sfor<0, G::P>([&](auto qr) {
+    constexpr int q = G::P - 1 - decltype(qr)::value;
+    if constexpr (q == 0 && G::P > 1) {
+      exchange<C, q + 1, q>(bufs, xc, sl, t, x, last_hook, post_hook);
+    } else if constexpr (q < G::P - 1) {
+      exchange<C, q + 1, q>(bufs, xc, sl, t, x, NoHook{}, post_hook);
+    }
+    if constexpr (q == 0) {
+      dif_pass_static<R, C::LOGE, G::G0>(x);
+    } else {
+      if constexpr (q == G::P - 1 && TOPREG) {
+        dif_pass_rt<R, G::tan01(q)>(x, TwRegs<R>{twr}, top_bits<LOGN, q>(t));
+      } else {
+        dif_pass_rt<R, G::tan01(q)>(
+            x, tw_smem<R, LOGN, q>(lowtab + G::tw_offset(q), t),
+            top_bits<LOGN, q>(t));
+      }
+    }
+  });
+}
+
+// ---------------------------------------------------------------------------
+// fused OLS kernel
+// ---------------------------------------------------------------------------
+template <class R>
+struct FusedArgs {
+  const Cpx<R>* x;
+  long long x_base, n_s;
+  const typename V16<R>::type* spec;  // engine layout
+  cudaTextureObject_t htex;           // texture over `spec` (H_TEX)
+  int n_fil, fchunk, pp_kind;
+  // segment grid (engine geometry, anchored at global sample 0): segment k
+  // reads the zero-extended window x[k*seg_len - t0 + origin, + N) and owns
+  // outputs [k*seg_len, (k+1)*seg_len) = in-place samples [t0, t0 + seg_len);
+  // this call writes outputs [g_lo, g_hi) of segments [k_lo, k_hi)
+  int t0, origin;
+  long long seg_len, k_lo, k_hi, g_lo, g_hi;
+  R pp_c;
+  Cpx<R>* out;
+  long long out_ld, out_base;
+  int dbg;  // tuning: bit 0 = predicate off the output stores
+};
+
+template <class C>
+__global__ void __launch_bounds__(C::THREADS, C::MINB)
+    fused_c2c_kernel(const FusedArgs<typename C::R> a) {
+  using R = typename C::R;
+  using G = typename C::G;
+  constexpr int LOGN = C::LOGN;
+  constexpr int E = C::E, T = C::T, P = C::P;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Cpx<R>* bufs = reinterpret_cast<Cpx<R>*>(smem_raw);
+  Tw<R>* lowtab = reinterpret_cast<Tw<R>*>(smem_raw + C::f_tab_off);
+  Cpx<R>* hbuf = reinterpret_cast<Cpx<R>*>(smem_raw + C::f_h_off);
+  uint64_t* hbar = reinterpret_cast<uint64_t*>(smem_raw + C::f_bar_off);
+
+  const int tid = threadIdx.x;
+  const int sl = tid / T;
+  const int t = tid % T;
+
+  // ---- work decomposition: items = (group of SEGS segments, filter chunk)
+  const long long nseg = a.k_hi - a.k_lo;
+  const long long ngroups = (nseg + C::SEGS - 1) / C::SEGS;
+  const int nfch = (a.n_fil + a.fchunk - 1) / a.fchunk;
+  const long long nitems = ngroups * nfch;
+
+  if constexpr (C::HM == H_TMA) {
+    if (tid == 0) {
+      mbar_init(&hbar[0], 1);
+      mbar_init(&hbar[1], 1);
+      fence_proxy_async();
+    }
+  }
+  build_tables<R, LOGN>(lowtab,
+                        C::TOPREG ? reinterpret_cast<Tw<R>*>(bufs) : nullptr);
+  __syncthreads();
+
+  // top-window twiddles: fixed per thread for the kernel lifetime
+  Tw<R> twr[15];
+  if constexpr (C::TOPREG) {
+    constexpr int q = P - 1;
+    const TwSmem<R> tt =
+        tw_smem<R, LOGN, q>(reinterpret_cast<const Tw<R>*>(bufs), t);
+    twr[0] = tt.get0();
+#pragma unroll
+    for (int pp = 1; pp < 8; ++pp) {
+      const TwPair<R> w = tt.get2(pp);
+      twr[2 * pp - 1] = w.a;
+      twr[2 * pp] = w.b;
+    }
+    __syncthreads();  // the exchange buffers are free from here on
+  }
+
+  // ---- filter-spectrum staging
+  // H_TMA: the (item, filter) pairs this CTA visits, in order; pair i lands
+  // in hbuf[i & 1] (TMA bulk copy issued one pair ahead by thread 0)
+  auto issue = [&](int f, int slot) {
+    if constexpr (C::HM == H_TMA) {
+      bulk_g2s(hbuf + size_t(slot) * G::N, a.spec + size_t(f) * C::VPT * T,
+               uint32_t(C::h_bytes), &hbar[slot]);
+    }
+  };
+  // H_ASYNC: this thread's VPT vectors of filter f -> its private slots
+  float4* hpriv = reinterpret_cast<float4*>(hbuf) + tid;
+  auto prefetch = [&](int f) {
+    if constexpr (C::HM == H_ASYNC) {
+      const float4* src = reinterpret_cast<const float4*>(a.spec) +
+                          size_t(f) * C::VPT * T + t;
+#pragma unroll
+      for (int u = 0; u < C::VPT; ++u)
+        cp_async16(hpriv + u * C::THREADS, src + u * T);
+      cp_async_commit();
+    }
+  };
+  if (blockIdx.x < nitems) {
+    const int f0 = int(blockIdx.x % nfch) * a.fchunk;
+    if (C::HM == H_TMA && tid == 0) issue(f0, 0);
+    prefetch(f0);
+  }
+
+  const R inv_n = R(1) / R(G::N);
+  int xc = 0;
+  unsigned hseq = 0;
+
+  for (long long it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const long long grp = it / nfch;
+    const int fc = int(it - grp * nfch);
+    const long long s = a.k_lo + grp * C::SEGS + sl;
+    const bool live = s < a.k_hi;
+    const long long g0 = s * a.seg_len;
+    // owned outputs o in [o_lo, o_hi) (clipped to this call's range)
+    const long long o_lo = a.g_lo > g0 ? a.g_lo - g0 : 0;
+    const long long o_hi = a.g_hi - g0 < a.seg_len ? a.g_hi - g0 : a.seg_len;
+    const unsigned span =
+        (!live || (a.dbg & 1) || o_hi <= o_lo) ? 0u : unsigned(o_hi - o_lo);
+    const long long w0 = g0 - a.t0 + a.origin;
+    const int f_lo = fc * a.fchunk;
+    const int f_hi = min(a.n_fil, f_lo + a.fchunk);
+    const long long nit = it + gridDim.x;
+    const int f_next_item = nit < nitems ? int(nit % nfch) * a.fchunk : -1;
+
+    // ---- segment staging: zero-extended window, top-window layout
+    // (_gather, _kernels_nb.py:206-215)
+    Cpx<R> x[E];
+    {
+      constexpr int q = P - 1;
+      const long long pb = w0 + G::thread_part(q, t);
+      const Cpx<R>* xp = a.x + (pb - a.x_base);
+      sfor<0, E>([&](auto ec) {
+        constexpr int e = decltype(ec)::value;
+        const long long gi = pb + G::elem_part(q, e);
+        if (live && (unsigned long long)gi < (unsigned long long)a.n_s) {
+          x[e] = xp[G::elem_part(q, e)];
+        } else {
+          x[e] = Cpx<R>{R(0), R(0)};
+        }
+      });
+    }
+    // ---- forward FFT (dif_fwd, _kernels_nb.py:11-28); the spectrum stays in
+    // registers with the inverse's 1/N and the scale post-process folded in.
+    // H_TMA: thread 0 makes sure this item's first spectrum has landed before
+    // the forward FFT's last barrier; everybody else learns it from the barrier
+    auto wait_cur = [&]() {
+      if constexpr (C::HM == H_TMA && P > 1) {
+        if (tid == 0) mbar_wait(&hbar[hseq & 1u], (hseq >> 1) & 1u);
+      }
+    };
+    forward_fft<C, C::TOPREG>(x, lowtab, twr, bufs, xc, sl, t, wait_cur);
+    {
+      const R sc = a.pp_kind == OLSB_PP_SCALE ? inv_n * a.pp_c : inv_n;
+#pragma unroll
+      for (int e = 0; e < E; ++e) x[e] = cscale(x[e], sc);
+    }
+
+    for (int f = f_lo; f < f_hi; ++f, ++hseq) {
+      const int slot = int(hseq & 1u);
+      const int f_next = f + 1 < f_hi ? f + 1 : f_next_item;
+      if constexpr (C::HM == H_TMA) {
+        if constexpr (P == 1) __syncthreads();  // no exchange barrier below
+        // prefetch the next (item, filter) pair into the other slot; its
+        // previous contents were consumed before the last exchange barrier
+        if (tid == 0 && f_next >= 0) issue(f_next, slot ^ 1);
+        if constexpr (P == 1) mbar_wait(&hbar[slot], (hseq >> 1) & 1u);
+      }
+      // ---- pointwise multiply, both operands bit-reversed
+      // (_kernels_nb.py:280-282)
+      Cpx<R> y[E];
+      auto mulh = [&](int u, float4 h) {
+        y[2 * u] = cmul(x[2 * u], Cpx<R>{R(h.x), R(h.y)});
+        y[2 * u + 1] = cmul(x[2 * u + 1], Cpx<R>{R(h.z), R(h.w)});
+      };
+      if constexpr (C::HM == H_TMA) {
+        const float4* hs =
+            reinterpret_cast<const float4*>(hbuf + size_t(slot) * G::N) + t;
+        sfor<0, C::VPT>([&](auto uc) {
+          constexpr int u = decltype(uc)::value;
+          mulh(u, hs[u * T]);
+        });
+      } else if constexpr (C::HM == H_TEX) {
+        const int hb = f * (C::VPT * T) + t;
+        sfor<0, C::VPT>([&](auto uc) {
+          constexpr int u = decltype(uc)::value;
+          mulh(u, tex1Dfetch<float4>(a.htex, hb + u * T));
+        });
+      } else if constexpr (C::HM == H_ASYNC) {
+        cp_async_wait_all();
+        sfor<0, C::VPT>([&](auto uc) {
+          constexpr int u = decltype(uc)::value;
+          mulh(u, hpriv[u * C::THREADS]);
+        });
+        if (f_next >= 0) prefetch(f_next);
+      } else {
+        const typename V16<R>::type* hs = a.spec + (size_t(f) * C::VPT) * T + t;
+        sfor<0, C::VPT>([&](auto uc) {
+          constexpr int u = decltype(uc)::value;
+          const auto h = __ldg(hs + u * T);
+          if constexpr (V16<R>::per == 2) {
+            mulh(u, h);
+          } else {
+            y[u] = cmul(x[u], Cpx<R>{h.x, h.y});
+          }
+        });
+      }
+      // ---- inverse FFT (dit_inv, _kernels_nb.py:31-51)
+      dit_pass_static<R, C::LOGE, G::G0>(y);
+      auto wait_next = [&]() {
+        if constexpr (C::HM == H_TMA) {
+          if (tid == 0 && f_next >= 0)
+            mbar_wait(&hbar[slot ^ 1], ((hseq + 1) >> 1) & 1u);
+        }
+      };
+      sfor<1, P>([&](auto qc) {
+        constexpr int q = decltype(qc)::value;
+        if constexpr (q == P - 1) {
+          exchange<C, q - 1, q>(bufs, xc, sl, t, y, wait_next);
+        } else {
+          exchange<C, q - 1, q>(bufs, xc, sl, t, y);
+        }
+        if constexpr (q == P - 1 && C::TOPREG) {
+          dit_pass_rt<R, G::tan01(q)>(y, TwRegs<R>{twr}, top_bits<LOGN, q>(t));
+        } else {
+          dit_pass_rt<R, G::tan01(q)>(
+              y, tw_smem<R, LOGN, q>(lowtab + G::tw_offset(q), t),
+              top_bits<LOGN, q>(t));
+        }
+      });
+      // ---- valid-sample writeback (_store kind 0/1, _kernels_nb.py:218-222):
+      // in-place sample p is output o = p - t0 of this segment, kept iff
+      // o_lo <= o < o_hi.  With the 32-aligned engine grid every warp store
+      // covers one aligned 256-byte chunk of the output row.
+      {
+        constexpr int q = P - 1;
+        const int o0 = G::thread_part(q, t) - a.t0;
+        const long long goff = (long long)f * a.out_ld + (g0 - a.out_base);
+        Cpx<R>* orow = a.out + goff + o0;
+        const int ol = int(o_lo);
+        sfor<0, E>([&](auto ec) {
+          constexpr int e = decltype(ec)::value;
+          constexpr int pe = G::elem_part(q, e);
+          st_cs_if(orow + pe, y[e], unsigned(o0 + pe - ol), span);
+        });
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// row transforms
+// ---------------------------------------------------------------------------
+template <class R>
+struct RowsArgs {
+  const Cpx<R>* in;
+  long long in_ld;  // row stride of `in` (elements)
+  int len;          // valid input columns (zero-padded to N)
+  int rows;
+  Cpx<R>* out_perm;                // may be null
+  typename V16<R>::type* out_dev;  // may be null
+};
+
+template <class C>
+__global__ void __launch_bounds__(C::THREADS)
+    fwd_rows_kernel(const RowsArgs<typename C::R> a) {
+  using R = typename C::R;
+  using G = typename C::G;
+  constexpr int E = C::E, T = C::T, P = C::P;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Tw<R>* tab = reinterpret_cast<Tw<R>*>(smem_raw);
+  Cpx<R>* bufs = reinterpret_cast<Cpx<R>*>(smem_raw + C::tab_bytes);
+  const int sl = threadIdx.x / T, t = threadIdx.x % T;
+  build_tables<R, C::LOGN>(tab, nullptr);
+  __syncthreads();
+  int xc = 0;
+  const int ngroups = (a.rows + C::SEGS - 1) / C::SEGS;
+  for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+    const int r = grp * C::SEGS + sl;
+    const bool live = r < a.rows;
+    Cpx<R> x[E];
+    {
+      constexpr int q = P - 1;
+      const int pb = G::thread_part(q, t);
+      sfor<0, E>([&](auto ec) {
+        constexpr int e = decltype(ec)::value;
+        const int p = pb + G::elem_part(q, e);
+        x[e] = (live && p < a.len) ? a.in[size_t(r) * a.in_ld + p]
+                                   : Cpx<R>{R(0), R(0)};
+      });
+    }
+    // every load of the group precedes any store (in-place safety)
+    __syncthreads();
+    forward_fft<C, false>(x, tab, nullptr, bufs, xc, sl, t);
+    if (live) {
+      if (a.out_perm) {
+        Cpx<R>* o = a.out_perm + size_t(r) * G::N + G::thread_part(0, t);
+#pragma unroll
+        for (int e = 0; e < E; ++e) o[e] = x[e];
+      }
+      if (a.out_dev) {
+        typename V16<R>::type* o = a.out_dev + size_t(r) * C::VPT * T + t;
+        if constexpr (!C::dbl) {
+#pragma unroll
+          for (int u = 0; u < C::VPT; ++u)
+            o[u * T] = make_float4(x[2 * u].re, x[2 * u].im, x[2 * u + 1].re,
+                                   x[2 * u + 1].im);
+        } else {
+#pragma unroll
+          for (int u = 0; u < C::VPT; ++u)
+            o[u * T] = make_double2(x[u].re, x[u].im);
+        }
+      }
+    }
+  }
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::THREADS)
+    inv_rows_kernel(const Cpx<typename C::R>* in, Cpx<typename C::R>* out,
+                    int rows) {
+  using R = typename C::R;
+  using G = typename C::G;
+  constexpr int LOGN = C::LOGN;
+  constexpr int E = C::E, T = C::T, P = C::P;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Tw<R>* tab = reinterpret_cast<Tw<R>*>(smem_raw);
+  Cpx<R>* bufs = reinterpret_cast<Cpx<R>*>(smem_raw + C::tab_bytes);
+  const int sl = threadIdx.x / T, t = threadIdx.x % T;
+  build_tables<R, LOGN>(tab, nullptr);
+  __syncthreads();
+  int xc = 0;
+  const R inv_n = R(1) / R(G::N);
+  const int ngroups = (rows + C::SEGS - 1) / C::SEGS;
+  for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+    const int r = grp * C::SEGS + sl;
+    const bool live = r < rows;
+    Cpx<R> y[E];
+    const Cpx<R>* src = in + size_t(r) * G::N + G::thread_part(0, t);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const Cpx<R> v = live ? src[e] : Cpx<R>{R(0), R(0)};
+      y[e] = Cpx<R>{v.re * inv_n, v.im * inv_n};
+    }
+    __syncthreads();
+    dit_pass_static<R, C::LOGE, G::G0>(y);
+    sfor<1, P>([&](auto qc) {
+      constexpr int q = decltype(qc)::value;
+      exchange<C, q - 1, q>(bufs, xc, sl, t, y);
+      dit_pass_rt<R, G::tan01(q)>(
+          y, tw_smem<R, LOGN, q>(tab + G::tw_offset(q), t),
+          top_bits<LOGN, q>(t));
+    });
+    if (live) {
+      constexpr int q = P - 1;
+      Cpx<R>* o = out + size_t(r) * G::N + G::thread_part(q, t);
+      sfor<0, E>([&](auto ec) {
+        constexpr int e = decltype(ec)::value;
+        o[G::elem_part(q, e)] = y[e];
+      });
+    }
+  }
+}
+
+template <class C>
+__global__ void perm_to_dev_kernel(const Cpx<typename C::R>* perm,
+                                   typename V16<typename C::R>::type* dev,
+                                   int rows) {
+  using R = typename C::R;
+  constexpr int T = C::T, VPT = C::VPT, per = V16<R>::per;
+  const long long total = (long long)rows * VPT * T;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+       i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / (VPT * T);
+    const int rem = int(i - r * VPT * T);
+    const int u = rem / T, t = rem % T;
+    const Cpx<R>* s = perm + r * C::G::N + t * C::E + u * per;
+    if constexpr (per == 2) {
+      dev[i] = make_float4(s[0].re, s[0].im, s[1].re, s[1].im);
+    } else {
+      dev[i] = make_double2(s[0].re, s[0].im);
+    }
+  }
+}
+
+}  // namespace olsb

@@ -78,8 +78,12 @@ struct Geo {
   static constexpr int G0 = LOGN - 4 * (P - 1);
   static constexpr int lo(int q) { return q == 0 ? 0 : LOGN - 4 * (P - q); }
   static constexpr int g(int q) { return q == 0 ? G0 : 4; }
-  // number of runtime twiddle entries of window q (15 per low-bit value l)
-  static constexpr int tw_entries(int q) { return q == 0 ? 0 : 15 << lo(q); }
+  // runtime twiddle entries of window q: 8 pair slots (16 entries, one
+  // unused) per low-bit value l, see twiddle_slot()
+  static constexpr int tw_entries(int q) { return q == 0 ? 0 : 16 << lo(q); }
+  // windows whose first two stages use the FMA (tangent) forms: the top
+  // window when lanes hold l's low 5 bits and its top 2 bits are warp bits
+  static constexpr bool tan01(int q) { return q == P - 1 && lo(q) >= 7; }
   static constexpr int tw_offset(int q) {
     int off = 0;
     for (int i = 1; i < q; ++i) off += tw_entries(i);
@@ -162,34 +166,125 @@ constexpr double static_c(int m) {
 constexpr double static_t(int m) {
   return static_form(m) == 3 ? -kCos8[m] / kSin8[m] : kSin8[m] / kCos8[m];
 }
-// runtime-window stages j >= 2 have a static form per k (SURVEY-free
-// derivation in DESIGN.md §3): theta in [pi k/2^j, pi (k+1)/2^j)
+// runtime-window stages j >= 2 have a static form per k (derivation in
+// DESIGN.md §3): theta in [pi k/2^j, pi (k+1)/2^j)
 constexpr bool rot_static(int j, int k) {
   return 4 * k >= (1 << j) && 4 * (k + 1) <= 3 * (1 << j);
 }
 
 // ---------------------------------------------------------------------------
+// packed fp32x2 arithmetic (sm_100a FADD2 / FMUL2 / FFMA2).  A complex<float>
+// is one aligned register pair; ptxas folds half swaps, per-half negation and
+// scalar broadcasts (`pk(x, x)`) into the instruction's operand modifiers, so
+// a complex butterfly costs half the issue slots of scalar code.  Device only;
+// the host (tests) and fp64 paths use the scalar formulas below.
+// ---------------------------------------------------------------------------
+#if defined(__CUDA_ARCH__)
+typedef unsigned long long u64;
+__device__ __forceinline__ u64 pk(float a, float b) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ u64 pk(Cpx<float> v) { return pk(v.re, v.im); }
+__device__ __forceinline__ Cpx<float> upk(u64 r) {
+  Cpx<float> v;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.re), "=f"(v.im) : "l"(r));
+  return v;
+}
+__device__ __forceinline__ u64 add2(u64 a, u64 b) {
+  u64 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
+  u64 d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
+  u64 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
+  u64 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+#define OLSB_PACKED(R) (std::is_same<R, float>::value)
+#else
+#define OLSB_PACKED(R) false
+#endif
+
+// complex product a * b
+template <class R>
+OLSB_HD Cpx<R> cmul(Cpx<R> a, Cpx<R> b) {
+#if defined(__CUDA_ARCH__)
+  if constexpr (OLSB_PACKED(R)) {
+    // a.re (b.re, b.im) + a.im (-b.im, b.re)
+    return upk(fma2(pk(-b.im, b.re), pk(a.im, a.im),
+                    mul2(pk(b.re, b.im), pk(a.re, a.re))));
+  }
+#endif
+  return Cpx<R>{fmaR(a.re, b.re, -a.im * b.im), fmaR(a.re, b.im, a.im * b.re)};
+}
+
+template <class R>
+OLSB_HD Cpx<R> cscale(Cpx<R> a, R s) {
+#if defined(__CUDA_ARCH__)
+  if constexpr (OLSB_PACKED(R)) return upk(mul2(pk(a), pk(s, s)));
+#endif
+  return Cpx<R>{a.re * s, a.im * s};
+}
+
+// ---------------------------------------------------------------------------
 // butterfly forms.  Inverse (DIT): a = u + w v, b = u - w v, w = e^{+i theta}.
 // Forward (DIF): a = u + v, b = (u - v) conj(w).
-// GOOD/ROT are the FMA ("tangent") forms: w v = c (v + i t v) is 2 FMA, and
-// the scale c fuses into the butterfly adds, so a twiddled DIT butterfly is
-// 6 FFMA instead of 4 mul + 4 add.  ROT handles |tan| > 1 by rotating w by
-// -pi/2 (the +i is a free swap/negate).
+// GOOD/ROT are the FMA ("tangent") forms: w v = c (v + i t v) is one FMA per
+// component, and the scale c fuses into the butterfly adds, so a twiddled
+// DIT butterfly is 6 FFMA (3 FFMA2) instead of 4 mul + 4 add.  ROT handles
+// |tan| > 1 by rotating w by -pi/2 (the +i is a free swap/negate).
 // ---------------------------------------------------------------------------
 template <class R>
 OLSB_HD void dit_one(Cpx<R>& u, Cpx<R>& v) {
+#if defined(__CUDA_ARCH__)
+  if constexpr (OLSB_PACKED(R)) {
+    const u64 U = pk(u), V = pk(v);
+    u = upk(add2(U, V));
+    v = upk(sub2(U, V));
+    return;
+  }
+#endif
   const Cpx<R> a{u.re + v.re, u.im + v.im};
   v = Cpx<R>{u.re - v.re, u.im - v.im};
   u = a;
 }
 template <class R>
 OLSB_HD void dit_i(Cpx<R>& u, Cpx<R>& v) {  // w = i: w v = (-v.im, v.re)
+#if defined(__CUDA_ARCH__)
+  if constexpr (OLSB_PACKED(R)) {
+    const u64 U = pk(u), IV = pk(-v.im, v.re);
+    u = upk(add2(U, IV));
+    v = upk(sub2(U, IV));
+    return;
+  }
+#endif
   const Cpx<R> a{u.re - v.im, u.im + v.re};
   v = Cpx<R>{u.re + v.im, u.im - v.re};
   u = a;
 }
 template <class R>
 OLSB_HD void dit_good(Cpx<R>& u, Cpx<R>& v, R c, R t) {
+#if defined(__CUDA_ARCH__)
+  if constexpr (OLSB_PACKED(R)) {
+    const u64 U = pk(u);
+    const u64 P = fma2(pk(v.im, v.re), pk(-t, t), pk(v));  // v + i t v
+    u = upk(fma2(P, pk(c, c), U));
+    v = upk(fma2(P, pk(-c, -c), U));
+    return;
+  }
+#endif
   const R pr = fmaR(-t, v.im, v.re);
   const R pi = fmaR(t, v.re, v.im);
   const Cpx<R> a{fmaR(c, pr, u.re), fmaR(c, pi, u.im)};
@@ -199,6 +294,16 @@ OLSB_HD void dit_good(Cpx<R>& u, Cpx<R>& v, R c, R t) {
 template <class R>
 OLSB_HD void dit_rot(Cpx<R>& u, Cpx<R>& v, R c, R t) {
   // w = i c (1 + i t): w v = i c p = (-c p.im, c p.re)
+#if defined(__CUDA_ARCH__)
+  if constexpr (OLSB_PACKED(R)) {
+    const u64 U = pk(u);
+    const Cpx<float> p =
+        upk(fma2(pk(v.im, v.re), pk(-t, t), pk(v)));  // v + i t v
+    u = upk(fma2(pk(-p.im, p.re), pk(c, c), U));
+    v = upk(fma2(pk(p.im, -p.re), pk(c, c), U));
+    return;
+  }
+#endif
   const R pr = fmaR(-t, v.im, v.re);
   const R pi = fmaR(t, v.re, v.im);
   const Cpx<R> a{fmaR(-c, pi, u.re), fmaR(c, pr, u.im)};
@@ -207,6 +312,16 @@ OLSB_HD void dit_rot(Cpx<R>& u, Cpx<R>& v, R c, R t) {
 }
 template <class R>
 OLSB_HD void dit_std(Cpx<R>& u, Cpx<R>& v, R c, R s) {
+#if defined(__CUDA_ARCH__)
+  if constexpr (OLSB_PACKED(R)) {
+    const u64 U = pk(u);
+    // v.re (c, s) + v.im (-s, c)
+    const u64 W = fma2(pk(-s, c), pk(v.im, v.im), mul2(pk(c, s), pk(v.re, v.re)));
+    u = upk(add2(U, W));
+    v = upk(sub2(U, W));
+    return;
+  }
+#endif
   const R wr = fmaR(v.re, c, -v.im * s);
   const R wi = fmaR(v.re, s, v.im * c);
   const Cpx<R> a{u.re + wr, u.im + wi};
@@ -218,6 +333,15 @@ template <class R>
 OLSB_HD void dif_one(Cpx<R>& u, Cpx<R>& v) { dit_one(u, v); }
 template <class R>
 OLSB_HD void dif_i(Cpx<R>& u, Cpx<R>& v) {  // conj(w) = -i: b = (d.im, -d.re)
+#if defined(__CUDA_ARCH__)
+  if constexpr (OLSB_PACKED(R)) {
+    const u64 U = pk(u), V = pk(v);
+    const Cpx<float> d = upk(sub2(U, V));
+    u = upk(add2(U, V));
+    v = Cpx<float>{d.im, -d.re};
+    return;
+  }
+#endif
   const R dr = u.re - v.re, di = u.im - v.im;
   u = Cpx<R>{u.re + v.re, u.im + v.im};
   v = Cpx<R>{di, -dr};
@@ -225,6 +349,16 @@ OLSB_HD void dif_i(Cpx<R>& u, Cpx<R>& v) {  // conj(w) = -i: b = (d.im, -d.re)
 template <class R>
 OLSB_HD void dif_good(Cpx<R>& u, Cpx<R>& v, R c, R t) {
   // conj(w) = c (1 - i t): b = c (d.re + t d.im, d.im - t d.re)
+#if defined(__CUDA_ARCH__)
+  if constexpr (OLSB_PACKED(R)) {
+    const u64 U = pk(u), V = pk(v);
+    const u64 D = sub2(U, V);
+    const Cpx<float> d = upk(D);
+    u = upk(add2(U, V));
+    v = upk(mul2(fma2(pk(d.im, -d.re), pk(t, t), D), pk(c, c)));
+    return;
+  }
+#endif
   const R dr = u.re - v.re, di = u.im - v.im;
   u = Cpx<R>{u.re + v.re, u.im + v.im};
   v = Cpx<R>{c * fmaR(t, di, dr), c * fmaR(-t, dr, di)};
@@ -232,6 +366,17 @@ OLSB_HD void dif_good(Cpx<R>& u, Cpx<R>& v, R c, R t) {
 template <class R>
 OLSB_HD void dif_rot(Cpx<R>& u, Cpx<R>& v, R c, R t) {
   // conj(w) = -i c (1 - i t): q = (d.re + t d.im, d.im - t d.re), b = -i c q
+#if defined(__CUDA_ARCH__)
+  if constexpr (OLSB_PACKED(R)) {
+    const u64 U = pk(u), V = pk(v);
+    const u64 D = sub2(U, V);
+    const Cpx<float> d = upk(D);
+    u = upk(add2(U, V));
+    const Cpx<float> q = upk(fma2(pk(d.im, -d.re), pk(t, t), D));
+    v = upk(mul2(pk(q.im, -q.re), pk(c, c)));
+    return;
+  }
+#endif
   const R dr = u.re - v.re, di = u.im - v.im;
   u = Cpx<R>{u.re + v.re, u.im + v.im};
   const R qr = fmaR(t, di, dr), qi = fmaR(-t, dr, di);
@@ -239,6 +384,17 @@ OLSB_HD void dif_rot(Cpx<R>& u, Cpx<R>& v, R c, R t) {
 }
 template <class R>
 OLSB_HD void dif_std(Cpx<R>& u, Cpx<R>& v, R c, R s) {
+#if defined(__CUDA_ARCH__)
+  if constexpr (OLSB_PACKED(R)) {
+    const u64 U = pk(u), V = pk(v);
+    const u64 D = sub2(U, V);
+    const Cpx<float> d = upk(D);
+    u = upk(add2(U, V));
+    // d conj(w) = d.re (c, -s) + d.im (s, c)
+    v = upk(fma2(pk(s, c), pk(d.im, d.im), mul2(pk(c, -s), pk(d.re, d.re))));
+    return;
+  }
+#endif
   const R dr = u.re - v.re, di = u.im - v.im;
   u = Cpx<R>{u.re + v.re, u.im + v.im};
   v = Cpx<R>{fmaR(dr, c, di * s), fmaR(di, c, -dr * s)};
@@ -297,55 +453,179 @@ OLSB_HD void dif_pass_static(Cpx<R>* x) {
   });
 }
 
-// Runtime windows (lo > 0): twiddle (j, k) is entry 2^j - 1 + k of the
-// thread's 15-entry set `tw(idx)`.  Stages j < 2 use STD entries, j >= 2 the
-// static GOOD/ROT form.
-template <class R, class TW>
-OLSB_HD void dit_pass_rt(Cpx<R>* x, const TW& tw) {
-  sfor<0, 4>([&](auto jc) {
+// Runtime windows (lo > 0).  Twiddle (j, k) of a thread is entry
+// idx = 2^j - 1 + k of its 15-entry set; accessors hand them out as idx 0
+// (get0) and pairs (2p - 1, 2p), p = 1..7 (get2) so a shared-memory table is
+// read with 128-bit loads.  Stages j >= 2 use the static GOOD/ROT form.
+// Stages j < 2 use STD, or with TAN01 the FMA forms, picked by `hb` = the top
+// two bits of l (warp-uniform where TAN01 is enabled):
+//   j = 0     : ROT iff hb in {1, 2}  (theta = pi x, x = l / 2^lo)
+//   j = 1, k=0: ROT iff hb >= 2       (theta = pi x / 2)
+//   j = 1, k=1: ROT iff hb <  2       (theta = pi (1 + x) / 2)
+template <class R>
+struct TwPair {
+  Tw<R> a, b;
+};
+
+template <class R, bool TAN01, class TW>
+OLSB_HD void dit_pass_rt(Cpx<R>* x, const TW& tw, int hb) {
+  // j = 0: pairs (2h, 2h + 1), twiddle idx 0
+  {
+    const Tw<R> w = tw.get0();
+    if constexpr (TAN01) {
+      if (hb == 1 || hb == 2) {
+        sfor<0, 8>([&](auto hc) {
+          constexpr int a = 2 * decltype(hc)::value;
+          dit_rot(x[a], x[a + 1], w.c, w.t);
+        });
+      } else {
+        sfor<0, 8>([&](auto hc) {
+          constexpr int a = 2 * decltype(hc)::value;
+          dit_good(x[a], x[a + 1], w.c, w.t);
+        });
+      }
+    } else {
+      sfor<0, 8>([&](auto hc) {
+        constexpr int a = 2 * decltype(hc)::value;
+        dit_std(x[a], x[a + 1], w.c, w.t);
+      });
+    }
+  }
+  // j = 1: k = 0 -> idx 1, k = 1 -> idx 2
+  {
+    const TwPair<R> w = tw.get2(1);
+    if constexpr (TAN01) {
+      if (hb >= 2) {
+        sfor<0, 4>([&](auto hc) {
+          constexpr int a = 4 * decltype(hc)::value;
+          dit_rot(x[a], x[a + 2], w.a.c, w.a.t);
+          dit_good(x[a + 1], x[a + 3], w.b.c, w.b.t);
+        });
+      } else {
+        sfor<0, 4>([&](auto hc) {
+          constexpr int a = 4 * decltype(hc)::value;
+          dit_good(x[a], x[a + 2], w.a.c, w.a.t);
+          dit_rot(x[a + 1], x[a + 3], w.b.c, w.b.t);
+        });
+      }
+    } else {
+      sfor<0, 4>([&](auto hc) {
+        constexpr int a = 4 * decltype(hc)::value;
+        dit_std(x[a], x[a + 2], w.a.c, w.a.t);
+        dit_std(x[a + 1], x[a + 3], w.b.c, w.b.t);
+      });
+    }
+  }
+  // j = 2, 3: static forms
+  sfor<2, 4>([&](auto jc) {
     constexpr int j = decltype(jc)::value;
-    sfor<0, (1 << j)>([&](auto kc) {
-      constexpr int k = decltype(kc)::value;
-      const Tw<R> w = tw((1 << j) - 1 + k);
-      sfor<0, (8 >> j)>([&](auto hc) {
-        constexpr int a = (decltype(hc)::value << (j + 1)) | k;
-        if constexpr (j < 2) {
-          dit_std(x[a], x[a | (1 << j)], w.c, w.t);
-        } else if constexpr (rot_static(j, k)) {
-          dit_rot(x[a], x[a | (1 << j)], w.c, w.t);
-        } else {
-          dit_good(x[a], x[a | (1 << j)], w.c, w.t);
-        }
+    sfor<(1 << (j - 1)), (1 << j)>([&](auto pc) {
+      constexpr int pp = decltype(pc)::value;
+      const TwPair<R> w = tw.get2(pp);
+      sfor<0, 2>([&](auto hc2) {
+        constexpr int idx = 2 * pp - 1 + decltype(hc2)::value;
+        constexpr int k = idx - ((1 << j) - 1);
+        const Tw<R> ww = decltype(hc2)::value == 0 ? w.a : w.b;
+        sfor<0, (8 >> j)>([&](auto hc) {
+          constexpr int a = (decltype(hc)::value << (j + 1)) | k;
+          if constexpr (rot_static(j, k)) {
+            dit_rot(x[a], x[a | (1 << j)], ww.c, ww.t);
+          } else {
+            dit_good(x[a], x[a | (1 << j)], ww.c, ww.t);
+          }
+        });
       });
     });
   });
 }
 
-template <class R, class TW>
-OLSB_HD void dif_pass_rt(Cpx<R>* x, const TW& tw) {
-  sfor<0, 4>([&](auto jr) {
+template <class R, bool TAN01, class TW>
+OLSB_HD void dif_pass_rt(Cpx<R>* x, const TW& tw, int hb) {
+  // j = 3, 2: static forms
+  sfor<0, 2>([&](auto jr) {
     constexpr int j = 3 - decltype(jr)::value;
-    sfor<0, (1 << j)>([&](auto kc) {
-      constexpr int k = decltype(kc)::value;
-      const Tw<R> w = tw((1 << j) - 1 + k);
-      sfor<0, (8 >> j)>([&](auto hc) {
-        constexpr int a = (decltype(hc)::value << (j + 1)) | k;
-        if constexpr (j < 2) {
-          dif_std(x[a], x[a | (1 << j)], w.c, w.t);
-        } else if constexpr (rot_static(j, k)) {
-          dif_rot(x[a], x[a | (1 << j)], w.c, w.t);
-        } else {
-          dif_good(x[a], x[a | (1 << j)], w.c, w.t);
-        }
+    sfor<(1 << (j - 1)), (1 << j)>([&](auto pc) {
+      constexpr int pp = decltype(pc)::value;
+      const TwPair<R> w = tw.get2(pp);
+      sfor<0, 2>([&](auto hc2) {
+        constexpr int idx = 2 * pp - 1 + decltype(hc2)::value;
+        constexpr int k = idx - ((1 << j) - 1);
+        const Tw<R> ww = decltype(hc2)::value == 0 ? w.a : w.b;
+        sfor<0, (8 >> j)>([&](auto hc) {
+          constexpr int a = (decltype(hc)::value << (j + 1)) | k;
+          if constexpr (rot_static(j, k)) {
+            dif_rot(x[a], x[a | (1 << j)], ww.c, ww.t);
+          } else {
+            dif_good(x[a], x[a | (1 << j)], ww.c, ww.t);
+          }
+        });
       });
     });
   });
+  // j = 1
+  {
+    const TwPair<R> w = tw.get2(1);
+    if constexpr (TAN01) {
+      if (hb >= 2) {
+        sfor<0, 4>([&](auto hc) {
+          constexpr int a = 4 * decltype(hc)::value;
+          dif_rot(x[a], x[a + 2], w.a.c, w.a.t);
+          dif_good(x[a + 1], x[a + 3], w.b.c, w.b.t);
+        });
+      } else {
+        sfor<0, 4>([&](auto hc) {
+          constexpr int a = 4 * decltype(hc)::value;
+          dif_good(x[a], x[a + 2], w.a.c, w.a.t);
+          dif_rot(x[a + 1], x[a + 3], w.b.c, w.b.t);
+        });
+      }
+    } else {
+      sfor<0, 4>([&](auto hc) {
+        constexpr int a = 4 * decltype(hc)::value;
+        dif_std(x[a], x[a + 2], w.a.c, w.a.t);
+        dif_std(x[a + 1], x[a + 3], w.b.c, w.b.t);
+      });
+    }
+  }
+  // j = 0
+  {
+    const Tw<R> w = tw.get0();
+    if constexpr (TAN01) {
+      if (hb == 1 || hb == 2) {
+        sfor<0, 8>([&](auto hc) {
+          constexpr int a = 2 * decltype(hc)::value;
+          dif_rot(x[a], x[a + 1], w.c, w.t);
+        });
+      } else {
+        sfor<0, 8>([&](auto hc) {
+          constexpr int a = 2 * decltype(hc)::value;
+          dif_good(x[a], x[a + 1], w.c, w.t);
+        });
+      }
+    } else {
+      sfor<0, 8>([&](auto hc) {
+        constexpr int a = 2 * decltype(hc)::value;
+        dif_std(x[a], x[a + 1], w.c, w.t);
+      });
+    }
+  }
 }
+
+// Table slot of twiddle idx: slot s = (idx + 1) / 2 holds the pair
+// (2s - 1, 2s) (slot 0: idx 0 and an unused half); half = 1 for even idx > 0.
+OLSB_HD constexpr int twiddle_slot(int idx) { return (idx + 1) >> 1; }
+OLSB_HD constexpr int twiddle_half(int idx) { return idx == 0 ? 0 : ((idx + 1) & 1); }
 
 // Value of runtime twiddle entry idx (j, k) for low bits l of window lo, in
 // double precision (theta / pi = (k 2^lo + l) / 2^(lo + j)).  Used to build
-// the shared-memory tables; forward uses conj implicitly.
-OLSB_HD void twiddle_entry(int lo, int idx, int l, double* c, double* t) {
+// the tables; the forward transform uses conj implicitly.  idx < 0 = unused.
+OLSB_HD void twiddle_entry(int lo, int idx, int l, bool tan01, double* c,
+                           double* t) {
+  if (idx < 0) {
+    *c = 0.0;
+    *t = 0.0;
+    return;
+  }
   int j = 0;
   while ((2 << j) - 1 <= idx) ++j;  // idx in [2^j - 1, 2^(j+1) - 1)
   const int k = idx - ((1 << j) - 1);
@@ -359,16 +639,34 @@ OLSB_HD void twiddle_entry(int lo, int idx, int l, double* c, double* t) {
   s = std::sin(th);
   co = std::cos(th);
 #endif
+  bool rot;
   if (j < 2) {
-    *c = co;
-    *t = s;
-  } else if (rot_static(j, k)) {
+    if (!tan01) {
+      *c = co;
+      *t = s;
+      return;
+    }
+    const int hb = lo >= 2 ? (l >> (lo - 2)) & 3 : 0;
+    rot = (j == 0) ? (hb == 1 || hb == 2) : (k == 0 ? hb >= 2 : hb < 2);
+  } else {
+    rot = rot_static(j, k);
+  }
+  if (rot) {
     *c = s;
     *t = -co / s;
   } else {
     *c = co;
     *t = s / co;
   }
+}
+
+// entry i of window lo's table -> (idx or -1, l)
+OLSB_HD void twiddle_decode(int lo, int i, int* idx, int* l) {
+  const int h = i & 1;
+  const int rest = i >> 1;
+  *l = rest & ((1 << lo) - 1);
+  const int sl = rest >> lo;
+  *idx = sl == 0 ? (h == 0 ? 0 : -1) : 2 * sl - 1 + h;
 }
 
 }  // namespace olsb

@@ -1,465 +1,21 @@
-// olsb_kernels.cu — sm_100a kernels and the C ABI of the OLS engine.
+// olsb_kernels.cu — launchers and the C ABI of the OLS engine (include/olsb.h).
 //
-// Kernels
-//   fused_c2c_kernel  the hot path: segment staging -> forward FFT -> per
-//                     filter {multiply, inverse FFT, valid-sample writeback}
-//                     (reference: _kernels_nb.py:265-285, ols.py:319-360)
-//   fwd_rows_kernel   forward transform of rows (filter spectra,
-//                     fft_forward_permuted); same passes as the fused kernel
-//   inv_rows_kernel   inverse transform of rows (fft_inverse_permuted)
-//   perm_to_dev_kernel  reference permuted layout -> engine layout
-//
-// One thread owns E = 16 samples of a segment; T = N / 16 threads form a
-// segment group, SEGS groups a CTA of 256 threads.  Samples move between
-// 4-bit windows through padded, bank-conflict-free shared memory (see
-// olsb_fft.cuh).  The whole filter loop runs with the segment spectrum held
-// in registers; filter spectra stream from L2 through L1 (every segment
-// group of the CTA reads the same spectrum in lockstep).
+// Device code lives in olsb_engine.cuh / olsb_fft.cuh.  Every entry point
+// validates its arguments, dispatches the runtime FFT length and precision to
+// a template instantiation and launches on the caller's stream.  Kernel
+// shapes (policies) are chosen per N from measurements;
+// OLSB_VARIANT=k overrides the N=2048/4096 fp32 policy for tuning sweeps.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
+#include <mutex>
 
 #include "olsb.h"
-#include "olsb_fft.cuh"
+#include "olsb_engine.cuh"
 
 namespace olsb {
-
-constexpr int kThreads = 256;
-
-// 16-byte vector type holding two complex<float> or one complex<double>
-template <class R>
-struct V16;
-template <>
-struct V16<float> {
-  using type = float4;
-  static constexpr int per = 2;  // complex per vector
-};
-template <>
-struct V16<double> {
-  using type = double2;
-  static constexpr int per = 1;
-};
-
-template <class R, int LOGN>
-struct Cfg {
-  using G = Geo<LOGN>;
-  using L = SmemLayout<R, LOGN>;
-  static constexpr bool dbl = std::is_same<R, double>::value;
-  static constexpr int E = G::E, T = G::T, P = G::P, LOGE = G::LOGE;
-  static constexpr int SEGS = (kThreads / T) > 0 ? (kThreads / T) : 1;
-  static constexpr int THREADS = SEGS * T;
-  static constexpr int NBUF = dbl ? 1 : 2;
-  static constexpr int VPT = E / V16<R>::per;  // 16-B vectors per thread (J)
-  // top-window twiddles kept in registers (float only; 30 registers)
-  static constexpr bool TOPREG = !dbl && P >= 2;
-  static constexpr int tab_elems = G::tw_total();
-  static constexpr size_t tab_bytes =
-      ((size_t(tab_elems) * sizeof(Tw<R>)) + 127) & ~size_t(127);
-  static constexpr size_t buf_elems = size_t(SEGS) * L::stride;
-  static constexpr size_t smem_bytes =
-      tab_bytes + (P >= 2 ? NBUF * buf_elems * sizeof(Cpx<R>) : 0);
-};
-
-// ---------------------------------------------------------------------------
-// shared-memory window I/O (addresses = per-thread base + immediates)
-// ---------------------------------------------------------------------------
-template <class R, int LOGN, int Q>
-__device__ __forceinline__ void smem_store(Cpx<R>* __restrict__ seg_buf, int t,
-                                           const Cpx<R>* x) {
-  using C = Cfg<R, LOGN>;
-  using G = typename C::G;
-  using L = typename C::L;
-  Cpx<R>* b = seg_buf + L::pos(G::thread_part(Q, t));
-  if constexpr (Q == 0 && !C::dbl && C::E >= 2) {
-    sfor<0, C::E / 2>([&](auto ec) {
-      constexpr int e = 2 * decltype(ec)::value;
-      constexpr int off = L::pos(G::elem_part(Q, e));
-      *reinterpret_cast<float4*>(b + off) =
-          make_float4(x[e].re, x[e].im, x[e + 1].re, x[e + 1].im);
-    });
-  } else {
-    sfor<0, C::E>([&](auto ec) {
-      constexpr int e = decltype(ec)::value;
-      constexpr int off = L::pos(G::elem_part(Q, e));
-      b[off] = x[e];
-    });
-  }
-}
-
-template <class R, int LOGN, int Q>
-__device__ __forceinline__ void smem_load(const Cpx<R>* __restrict__ seg_buf,
-                                          int t, Cpx<R>* x) {
-  using C = Cfg<R, LOGN>;
-  using G = typename C::G;
-  using L = typename C::L;
-  const Cpx<R>* b = seg_buf + L::pos(G::thread_part(Q, t));
-  if constexpr (Q == 0 && !C::dbl && C::E >= 2) {
-    sfor<0, C::E / 2>([&](auto ec) {
-      constexpr int e = 2 * decltype(ec)::value;
-      constexpr int off = L::pos(G::elem_part(Q, e));
-      const float4 v = *reinterpret_cast<const float4*>(b + off);
-      x[e] = Cpx<R>{v.x, v.y};
-      x[e + 1] = Cpx<R>{v.z, v.w};
-    });
-  } else {
-    sfor<0, C::E>([&](auto ec) {
-      constexpr int e = decltype(ec)::value;
-      constexpr int off = L::pos(G::elem_part(Q, e));
-      x[e] = b[off];
-    });
-  }
-}
-
-// twiddle tables for windows 1..P-1 (double-precision math, rounded once)
-template <class R, int LOGN>
-__device__ void build_tables(Tw<R>* tab) {
-  using G = Geo<LOGN>;
-  sfor<1, G::P>([&](auto qc) {
-    constexpr int q = decltype(qc)::value;
-    constexpr int lo = G::lo(q);
-    constexpr int cnt = G::tw_entries(q);
-    constexpr int off = G::tw_offset(q);
-    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-      double c, t;
-      twiddle_entry(lo, i >> lo, i & ((1 << lo) - 1), &c, &t);
-      tab[off + i] = Tw<R>{R(c), R(t)};
-    }
-  });
-}
-
-// accessor of the thread's 15 runtime twiddles of window q
-template <class R>
-struct TwSmem {
-  const Tw<R>* base;  // tab + off + l
-  int lstride;        // 2^lo
-  __device__ __forceinline__ Tw<R> operator()(int idx) const {
-    return base[idx * lstride];
-  }
-};
-template <class R>
-struct TwRegs {
-  const Tw<R>* r;
-  __device__ __forceinline__ Tw<R> operator()(int idx) const { return r[idx]; }
-};
-
-// exchange: write window QW, barrier, read window QR
-template <class R, int LOGN, int QW, int QR>
-__device__ __forceinline__ void exchange(Cpx<R>* bufs, int& xc, int sl, int t,
-                                         Cpx<R>* x) {
-  using C = Cfg<R, LOGN>;
-  Cpx<R>* buf = bufs + (C::NBUF == 2 ? (xc & 1) * C::buf_elems : 0) +
-                size_t(sl) * C::L::stride;
-  if constexpr (C::NBUF == 1) __syncthreads();
-  smem_store<R, LOGN, QW>(buf, t, x);
-  __syncthreads();
-  smem_load<R, LOGN, QR>(buf, t, x);
-  ++xc;
-}
-
-// full forward transform: x holds window P-1 on entry, window 0 (J) on exit
-template <class R, int LOGN>
-__device__ __forceinline__ void forward_fft(Cpx<R>* x, const Tw<R>* tab,
-                                            Cpx<R>* bufs, int& xc, int sl,
-                                            int t) {
-  using C = Cfg<R, LOGN>;
-  using G = typename C::G;
-  sfor<0, G::P>([&](auto qr) {
-    constexpr int q = G::P - 1 - decltype(qr)::value;
-    if constexpr (q < G::P - 1) exchange<R, LOGN, q + 1, q>(bufs, xc, sl, t, x);
-    if constexpr (q == 0) {
-      dif_pass_static<R, C::LOGE, G::G0>(x);
-    } else {
-      constexpr int lo = G::lo(q);
-      const TwSmem<R> tw{tab + G::tw_offset(q) + G::low_bits(q, t), 1 << lo};
-      dif_pass_rt<R>(x, tw);
-    }
-  });
-}
-
-// ---------------------------------------------------------------------------
-// fused OLS kernel
-// ---------------------------------------------------------------------------
-template <class R>
-struct FusedArgs {
-  const Cpx<R>* x;
-  long long x_base, n_s;
-  const typename V16<R>::type* spec;  // engine layout
-  int n_fil, fchunk, t0, pp_kind;
-  long long l_eff, win_off, seg_lo, seg_hi;
-  R pp_c;
-  Cpx<R>* out;
-  long long out_ld, out_base;
-};
-
-template <class R, int LOGN>
-__global__ void __launch_bounds__(Cfg<R, LOGN>::THREADS)
-    fused_c2c_kernel(const FusedArgs<R> a) {
-  using C = Cfg<R, LOGN>;
-  using G = typename C::G;
-  constexpr int E = C::E, T = C::T, P = C::P;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  Tw<R>* tab = reinterpret_cast<Tw<R>*>(smem_raw);
-  Cpx<R>* bufs = reinterpret_cast<Cpx<R>*>(smem_raw + C::tab_bytes);
-
-  const int tid = threadIdx.x;
-  const int sl = tid / T;
-  const int t = tid % T;
-
-  build_tables<R, LOGN>(tab);
-  __syncthreads();
-
-  // top-window (inverse) twiddles: fixed per thread for the kernel lifetime
-  Tw<R> twr[15];
-  if constexpr (C::TOPREG) {
-    constexpr int q = P - 1;
-    const Tw<R>* base = tab + G::tw_offset(q) + G::low_bits(q, t);
-#pragma unroll
-    for (int i = 0; i < 15; ++i) twr[i] = base[i << G::lo(q)];
-  }
-
-  const long long nseg = a.seg_hi - a.seg_lo;
-  const long long ngroups = (nseg + C::SEGS - 1) / C::SEGS;
-  const int nfch = (a.n_fil + a.fchunk - 1) / a.fchunk;
-  const long long nitems = ngroups * nfch;
-  const R inv_n = R(1) / R(G::N);
-  int xc = 0;
-
-  for (long long it = blockIdx.x; it < nitems; it += gridDim.x) {
-    const long long grp = it / nfch;
-    const int fc = int(it - grp * nfch);
-    const long long s = a.seg_lo + grp * C::SEGS + sl;
-    const bool live = s < a.seg_hi;
-    const long long g0 = s * a.l_eff;
-    const long long span =
-        live ? (a.l_eff < a.n_s - g0 ? a.l_eff : a.n_s - g0) : 0;
-    const long long w0 = g0 + a.win_off;
-
-    // ---- segment staging: zero-extended window, top-window layout
-    // (_gather, _kernels_nb.py:206-215)
-    Cpx<R> x[E];
-    {
-      constexpr int q = P - 1;
-      const long long pb = w0 + G::thread_part(q, t);
-      sfor<0, E>([&](auto ec) {
-        constexpr int e = decltype(ec)::value;
-        const long long gi = pb + G::elem_part(q, e);
-        if (live && gi >= 0 && gi < a.n_s) {
-          x[e] = a.x[gi - a.x_base];
-        } else {
-          x[e] = Cpx<R>{R(0), R(0)};
-        }
-      });
-    }
-    // ---- forward FFT (dif_fwd, _kernels_nb.py:11-28), spectrum kept in
-    // registers with the inverse's 1/N folded in
-    forward_fft<R, LOGN>(x, tab, bufs, xc, sl, t);
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      x[e].re *= inv_n;
-      x[e].im *= inv_n;
-    }
-
-    const int f_lo = fc * a.fchunk;
-    const int f_hi = min(a.n_fil, f_lo + a.fchunk);
-    for (int f = f_lo; f < f_hi; ++f) {
-      // ---- pointwise multiply, both operands bit-reversed
-      // (_kernels_nb.py:280-282)
-      Cpx<R> y[E];
-      const typename V16<R>::type* hs =
-          a.spec + (size_t(f) * C::VPT) * T + t;
-      if constexpr (!C::dbl) {
-        sfor<0, C::VPT>([&](auto uc) {
-          constexpr int u = decltype(uc)::value;
-          const float4 h = __ldg(reinterpret_cast<const float4*>(hs) + u * T);
-          const Cpx<R> s0 = x[2 * u], s1 = x[2 * u + 1];
-          y[2 * u] = Cpx<R>{fmaR(s0.re, h.x, -s0.im * h.y),
-                            fmaR(s0.re, h.y, s0.im * h.x)};
-          y[2 * u + 1] = Cpx<R>{fmaR(s1.re, h.z, -s1.im * h.w),
-                                fmaR(s1.re, h.w, s1.im * h.z)};
-        });
-      } else {
-        sfor<0, C::VPT>([&](auto uc) {
-          constexpr int u = decltype(uc)::value;
-          const double2 h = __ldg(reinterpret_cast<const double2*>(hs) + u * T);
-          const Cpx<R> s0 = x[u];
-          y[u] = Cpx<R>{fmaR(s0.re, h.x, -s0.im * h.y),
-                        fmaR(s0.re, h.y, s0.im * h.x)};
-        });
-      }
-      // ---- inverse FFT (dit_inv, _kernels_nb.py:31-51)
-      dit_pass_static<R, C::LOGE, G::G0>(y);
-      sfor<1, P>([&](auto qc) {
-        constexpr int q = decltype(qc)::value;
-        exchange<R, LOGN, q - 1, q>(bufs, xc, sl, t, y);
-        if constexpr (q == P - 1 && C::TOPREG) {
-          dit_pass_rt<R>(y, TwRegs<R>{twr});
-        } else {
-          constexpr int lo = G::lo(q);
-          const TwSmem<R> tw{tab + G::tw_offset(q) + G::low_bits(q, t),
-                             1 << lo};
-          dit_pass_rt<R>(y, tw);
-        }
-      });
-      // ---- valid-sample writeback (_store kind 0/1, _kernels_nb.py:218-222)
-      {
-        constexpr int q = P - 1;
-        const long long ob = G::thread_part(q, t) - a.t0;
-        Cpx<R>* orow = a.out + f * a.out_ld + g0 - a.out_base;
-        const bool scale = a.pp_kind == OLSB_PP_SCALE;
-        sfor<0, E>([&](auto ec) {
-          constexpr int e = decltype(ec)::value;
-          const long long o = ob + G::elem_part(q, e);
-          if (live && o >= 0 && o < span) {
-            Cpx<R> v = y[e];
-            if (scale) {
-              v.re *= a.pp_c;
-              v.im *= a.pp_c;
-            }
-            if constexpr (!C::dbl) {
-              __stcs(reinterpret_cast<float2*>(orow + o),
-                     make_float2(v.re, v.im));
-            } else {
-              __stcs(reinterpret_cast<double2*>(orow + o),
-                     make_double2(v.re, v.im));
-            }
-          }
-        });
-      }
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// row transforms
-// ---------------------------------------------------------------------------
-template <class R>
-struct RowsArgs {
-  const Cpx<R>* in;
-  long long in_ld;  // row stride of `in` (elements)
-  int len;          // valid input columns (zero-padded to N)
-  int rows;
-  Cpx<R>* out_perm;  // may be null
-  typename V16<R>::type* out_dev;  // may be null
-};
-
-template <class R, int LOGN>
-__global__ void __launch_bounds__(Cfg<R, LOGN>::THREADS)
-    fwd_rows_kernel(const RowsArgs<R> a) {
-  using C = Cfg<R, LOGN>;
-  using G = typename C::G;
-  constexpr int E = C::E, T = C::T, P = C::P;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  Tw<R>* tab = reinterpret_cast<Tw<R>*>(smem_raw);
-  Cpx<R>* bufs = reinterpret_cast<Cpx<R>*>(smem_raw + C::tab_bytes);
-  const int sl = threadIdx.x / T, t = threadIdx.x % T;
-  build_tables<R, LOGN>(tab);
-  __syncthreads();
-  int xc = 0;
-  const int ngroups = (a.rows + C::SEGS - 1) / C::SEGS;
-  for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
-    const int r = grp * C::SEGS + sl;
-    const bool live = r < a.rows;
-    Cpx<R> x[E];
-    {
-      constexpr int q = P - 1;
-      const int pb = G::thread_part(q, t);
-      sfor<0, E>([&](auto ec) {
-        constexpr int e = decltype(ec)::value;
-        const int p = pb + G::elem_part(q, e);
-        x[e] = (live && p < a.len) ? a.in[size_t(r) * a.in_ld + p]
-                                   : Cpx<R>{R(0), R(0)};
-      });
-    }
-    // every load of the group precedes any store (in-place safety)
-    __syncthreads();
-    forward_fft<R, LOGN>(x, tab, bufs, xc, sl, t);
-    if (live) {
-      if (a.out_perm) {
-        Cpx<R>* o = a.out_perm + size_t(r) * G::N + G::thread_part(0, t);
-#pragma unroll
-        for (int e = 0; e < E; ++e) o[e] = x[e];
-      }
-      if (a.out_dev) {
-        typename V16<R>::type* o = a.out_dev + size_t(r) * C::VPT * T + t;
-        if constexpr (!C::dbl) {
-#pragma unroll
-          for (int u = 0; u < C::VPT; ++u)
-            o[u * T] = make_float4(x[2 * u].re, x[2 * u].im, x[2 * u + 1].re,
-                                   x[2 * u + 1].im);
-        } else {
-#pragma unroll
-          for (int u = 0; u < C::VPT; ++u) o[u * T] = make_double2(x[u].re, x[u].im);
-        }
-      }
-    }
-  }
-}
-
-template <class R, int LOGN>
-__global__ void __launch_bounds__(Cfg<R, LOGN>::THREADS)
-    inv_rows_kernel(const Cpx<R>* in, Cpx<R>* out, int rows) {
-  using C = Cfg<R, LOGN>;
-  using G = typename C::G;
-  constexpr int E = C::E, T = C::T, P = C::P;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  Tw<R>* tab = reinterpret_cast<Tw<R>*>(smem_raw);
-  Cpx<R>* bufs = reinterpret_cast<Cpx<R>*>(smem_raw + C::tab_bytes);
-  const int sl = threadIdx.x / T, t = threadIdx.x % T;
-  build_tables<R, LOGN>(tab);
-  __syncthreads();
-  int xc = 0;
-  const R inv_n = R(1) / R(G::N);
-  const int ngroups = (rows + C::SEGS - 1) / C::SEGS;
-  for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
-    const int r = grp * C::SEGS + sl;
-    const bool live = r < rows;
-    Cpx<R> y[E];
-    const Cpx<R>* src = in + size_t(r) * G::N + G::thread_part(0, t);
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const Cpx<R> v = live ? src[e] : Cpx<R>{R(0), R(0)};
-      y[e] = Cpx<R>{v.re * inv_n, v.im * inv_n};
-    }
-    __syncthreads();
-    dit_pass_static<R, C::LOGE, G::G0>(y);
-    sfor<1, P>([&](auto qc) {
-      constexpr int q = decltype(qc)::value;
-      exchange<R, LOGN, q - 1, q>(bufs, xc, sl, t, y);
-      const TwSmem<R> tw{tab + G::tw_offset(q) + G::low_bits(q, t),
-                         1 << G::lo(q)};
-      dit_pass_rt<R>(y, tw);
-    });
-    if (live) {
-      constexpr int q = P - 1;
-      Cpx<R>* o = out + size_t(r) * G::N + G::thread_part(q, t);
-      sfor<0, E>([&](auto ec) {
-        constexpr int e = decltype(ec)::value;
-        o[G::elem_part(q, e)] = y[e];
-      });
-    }
-  }
-}
-
-template <class R, int LOGN>
-__global__ void perm_to_dev_kernel(const Cpx<R>* perm,
-                                   typename V16<R>::type* dev, int rows) {
-  using C = Cfg<R, LOGN>;
-  constexpr int T = C::T, VPT = C::VPT, per = V16<R>::per;
-  const long long total = (long long)rows * VPT * T;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-       i < total; i += (long long)gridDim.x * blockDim.x) {
-    const long long r = i / (VPT * T);
-    const int rem = int(i - r * VPT * T);
-    const int u = rem / T, t = rem % T;
-    const Cpx<R>* s = perm + r * Geo<LOGN>::N + t * C::E + u * per;
-    if constexpr (per == 2) {
-      dev[i] = make_float4(s[0].re, s[0].im, s[1].re, s[1].im);
-    } else {
-      dev[i] = make_double2(s[0].re, s[0].im);
-    }
-  }
-}
 
 // ---------------------------------------------------------------------------
 // launch helpers
@@ -486,28 +42,138 @@ int prepare(K kernel, size_t smem, int threads, int* resident) {
 
 static int g_filter_chunk = 0;
 
+// Texture objects over engine-layout spectra (H_TEX), cached per
+// (device, pointer, size); creating one costs microseconds, so a FilterSet
+// reused across calls pays it once.
+struct TexKey {
+  int dev;
+  const void* ptr;
+  size_t bytes;
+  cudaTextureObject_t tex;
+};
+static std::mutex g_tex_mu;
+static TexKey g_tex_cache[64];
+static int g_tex_n = 0;
+
+inline int spectra_texture(const void* ptr, size_t bytes,
+                           cudaTextureObject_t* out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_tex_mu);
+  for (int i = 0; i < g_tex_n; ++i) {
+    if (g_tex_cache[i].dev == dev && g_tex_cache[i].ptr == ptr &&
+        g_tex_cache[i].bytes == bytes) {
+      *out = g_tex_cache[i].tex;
+      return 0;
+    }
+  }
+  cudaResourceDesc rd = {};
+  rd.resType = cudaResourceTypeLinear;
+  rd.res.linear.devPtr = const_cast<void*>(ptr);
+  rd.res.linear.desc = cudaCreateChannelDesc<float4>();
+  rd.res.linear.sizeInBytes = bytes;
+  cudaTextureDesc td = {};
+  td.readMode = cudaReadModeElementType;
+  cudaTextureObject_t tex = 0;
+  cudaError_t e = cudaCreateTextureObject(&tex, &rd, &td, nullptr);
+  if (e != cudaSuccess) return int(e);
+  // a freed-and-reused allocation with the same address keeps a valid
+  // descriptor (linear textures hold only pointer + size)
+  if (g_tex_n == 64) {
+    cudaDestroyTextureObject(g_tex_cache[0].tex);
+    for (int i = 1; i < 64; ++i) g_tex_cache[i - 1] = g_tex_cache[i];
+    g_tex_n = 63;
+  }
+  g_tex_cache[g_tex_n++] = TexKey{dev, ptr, bytes, tex};
+  *out = tex;
+  return 0;
+}
+
+// default fused-kernel policy per (precision, N)
 template <class R, int LOGN>
-int launch_fused(FusedArgs<R> a, cudaStream_t st) {
-  using C = Cfg<R, LOGN>;
-  auto kern = fused_c2c_kernel<R, LOGN>;
+struct DefaultPolicy {
+  static constexpr bool dbl = std::is_same<R, double>::value;
+  static constexpr int T = Geo<LOGN>::T;
+  // fp32: one 128-thread group of segments per CTA, one exchange buffer,
+  // spectra through the TEX path, 16 warps per SM
+  static constexpr int SEGS = dbl ? std::max(1, 256 / T) : std::max(1, 128 / T);
+  using type = KCfg<R, LOGN, SEGS, 1, dbl ? H_LDG : H_TEX, 0,
+                    dbl ? 1 : std::max(1, 512 / (SEGS * T))>;
+};
+
+// tuning variants for fp32 N >= 2048 (OLSB_VARIANT)
+template <int LOGN, int V>
+struct Variant {
+  static constexpr int T = Geo<LOGN>::T;
+  // {SEGS, NBUF, HM, BAR, MINB (CTAs/SM at T = 128)}
+  static constexpr int tab[8][5] = {
+      {1, 1, H_TEX, 0, 4}, {1, 2, H_TEX, 0, 4}, {2, 2, H_TEX, 1, 2},
+      {1, 1, H_TMA, 0, 4}, {1, 2, H_LDG, 0, 4}, {2, 1, H_TEX, 0, 2},
+      {2, 2, H_TMA, 0, 2}, {1, 1, H_LDG, 0, 4}};
+  static constexpr int segs = tab[V][0];
+  static constexpr int minb = std::max(1, tab[V][4] * 128 / T);
+  using type = KCfg<float, LOGN, segs, tab[V][1], tab[V][2], tab[V][3], minb>;
+};
+
+inline int debug_env() {
+  static int v = [] {
+    const char* e = getenv("OLSB_DEBUG");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+inline int variant_env() {
+  static int v = [] {
+    const char* e = getenv("OLSB_VARIANT");
+    return e ? atoi(e) : -1;
+  }();
+  return v;
+}
+
+template <class C>
+int launch_fused_cfg(FusedArgs<typename C::R> a, cudaStream_t st) {
+  auto kern = fused_c2c_kernel<C>;
   int resident = 0;
-  int rc = prepare(kern, C::smem_bytes, C::THREADS, &resident);
+  int rc = prepare(kern, C::f_smem_bytes, C::THREADS, &resident);
   if (rc) return rc;
+  if constexpr (C::HM == H_TEX) {
+    rc = spectra_texture(a.spec, size_t(a.n_fil) * C::VPT * C::T * 16, &a.htex);
+    if (rc) return rc;
+  }
   a.fchunk = (g_filter_chunk > 0 && g_filter_chunk < a.n_fil) ? g_filter_chunk
                                                               : a.n_fil;
-  const long long nseg = a.seg_hi - a.seg_lo;
+  const long long nseg = a.k_hi - a.k_lo;
   const long long ngroups = (nseg + C::SEGS - 1) / C::SEGS;
   const long long nitems = ngroups * ((a.n_fil + a.fchunk - 1) / a.fchunk);
   const int grid = int(std::min<long long>(nitems, resident));
   if (grid <= 0) return 0;
-  kern<<<grid, C::THREADS, C::smem_bytes, st>>>(a);
+  kern<<<grid, C::THREADS, C::f_smem_bytes, st>>>(a);
   return int(cudaGetLastError());
 }
 
 template <class R, int LOGN>
+int launch_fused(FusedArgs<R> a, cudaStream_t st) {
+  if constexpr (std::is_same<R, float>::value && LOGN >= 11) {
+    switch (variant_env()) {
+      case 0: return launch_fused_cfg<typename Variant<LOGN, 0>::type>(a, st);
+      case 1: return launch_fused_cfg<typename Variant<LOGN, 1>::type>(a, st);
+      case 2: return launch_fused_cfg<typename Variant<LOGN, 2>::type>(a, st);
+      case 3: return launch_fused_cfg<typename Variant<LOGN, 3>::type>(a, st);
+      case 4: return launch_fused_cfg<typename Variant<LOGN, 4>::type>(a, st);
+      case 5: return launch_fused_cfg<typename Variant<LOGN, 5>::type>(a, st);
+      case 6: return launch_fused_cfg<typename Variant<LOGN, 6>::type>(a, st);
+      case 7: return launch_fused_cfg<typename Variant<LOGN, 7>::type>(a, st);
+      default: break;
+    }
+  }
+  return launch_fused_cfg<typename DefaultPolicy<R, LOGN>::type>(a, st);
+}
+
+template <class R, int LOGN>
 int launch_fwd_rows(RowsArgs<R> a, cudaStream_t st) {
-  using C = Cfg<R, LOGN>;
-  auto kern = fwd_rows_kernel<R, LOGN>;
+  using C = RowCfg<R, LOGN>;
+  auto kern = fwd_rows_kernel<C>;
   int resident = 0;
   int rc = prepare(kern, C::smem_bytes, C::THREADS, &resident);
   if (rc) return rc;
@@ -520,8 +186,8 @@ int launch_fwd_rows(RowsArgs<R> a, cudaStream_t st) {
 
 template <class R, int LOGN>
 int launch_inv_rows(const Cpx<R>* in, Cpx<R>* out, int rows, cudaStream_t st) {
-  using C = Cfg<R, LOGN>;
-  auto kern = inv_rows_kernel<R, LOGN>;
+  using C = RowCfg<R, LOGN>;
+  auto kern = inv_rows_kernel<C>;
   int resident = 0;
   int rc = prepare(kern, C::smem_bytes, C::THREADS, &resident);
   if (rc) return rc;
@@ -535,11 +201,11 @@ int launch_inv_rows(const Cpx<R>* in, Cpx<R>* out, int rows, cudaStream_t st) {
 template <class R, int LOGN>
 int launch_perm_to_dev(const Cpx<R>* perm, void* dev, int rows,
                        cudaStream_t st) {
-  const long long total =
-      (long long)rows * Cfg<R, LOGN>::VPT * Cfg<R, LOGN>::T;
+  using C = RowCfg<R, LOGN>;
+  const long long total = (long long)rows * C::VPT * C::T;
   if (total == 0) return 0;
   const int grid = int(std::min<long long>((total + 255) / 256, 4096));
-  perm_to_dev_kernel<R, LOGN><<<grid, 256, 0, st>>>(
+  perm_to_dev_kernel<C><<<grid, 256, 0, st>>>(
       perm, reinterpret_cast<typename V16<R>::type*>(dev), rows);
   return int(cudaGetLastError());
 }
@@ -675,46 +341,112 @@ int olsb_spectra_perm_to_dev(const void* spectra_perm, int n_fil, int n,
   });
 }
 
-int olsb_fused_c2c(const void* x, int64_t x_base, int64_t n_s,
-                   const void* spectra_dev, int n_fil, int n, int m,
-                   int origin, int64_t l_eff, int t0, int64_t win_off,
-                   int64_t seg_lo, int64_t seg_hi, int pp_kind, double pp_c,
-                   void* out, int64_t out_ld, int64_t out_base,
-                   int precision, void* stream) {
+// Engine segment grid for the reference geometry (t0, l_eff) at length n:
+// valid in-place samples [t0, t0 + l_eff) of every segment.  For n >= 512
+// the engine discards up to the next multiple of 32 and keeps a multiple of
+// 32 samples, so every warp store writes one aligned 256-byte chunk; the grid
+// is anchored at sample 0, so any split of the output range is bit-identical.
+static void engine_grid(int n, int t0, long long l_eff, int* t0e,
+                        long long* le) {
+  *t0e = t0;
+  *le = l_eff;
+  if (n < 512) return;
+  const int ta = (t0 + 31) & ~31;
+  const long long la = ((long long)t0 + l_eff - ta) & ~31LL;
+  if (la >= 32 && la * 100 >= l_eff * 97) {
+    *t0e = ta;
+    *le = la;
+  }
+}
+
+static int fused_range(const void* x, int64_t x_base, int64_t n_s,
+                       const void* spectra_dev, int n_fil, int n, int t0,
+                       int origin, int64_t l_eff, int64_t g_lo, int64_t g_hi,
+                       int pp_kind, double pp_c, void* out, int64_t out_ld,
+                       int64_t out_base, int precision, void* stream) {
   const int logn = log2_of(n);
   if (logn < 0) return OLSB_E_BAD_LENGTH;
   if (pp_kind != OLSB_PP_NONE && pp_kind != OLSB_PP_SCALE)
     return OLSB_E_UNSUPPORTED;
-  if (n_s < 1 || n_fil < 0 || m < 1 || m > n || origin < 0 || origin >= m ||
-      seg_lo < 0 || seg_hi < seg_lo)
-    return OLSB_E_BAD_ARG;
+  if (n_s < 1 || n_fil < 0 || g_lo < 0 || g_hi < g_lo) return OLSB_E_BAD_ARG;
   if (l_eff < 1 || t0 < 0 || t0 + l_eff > n) return OLSB_E_GEOMETRY;
-  if (n_fil == 0 || seg_hi == seg_lo) return 0;
+  if (g_hi > n_s) g_hi = n_s;
+  if (n_fil == 0 || g_hi <= g_lo) return 0;
   if (!x || !spectra_dev || !out) return OLSB_E_BAD_ARG;
+  int t0e;
+  long long le;
+  engine_grid(n, t0, l_eff, &t0e, &le);
   return dispatch_prec(precision, [&](auto rv) {
     using R = decltype(rv);
     return dispatch_n<R>(logn, [&](auto lc) {
-      FusedArgs<R> a;
+      FusedArgs<R> a = {};
       a.x = static_cast<const Cpx<R>*>(x);
       a.x_base = x_base;
       a.n_s = n_s;
       a.spec = static_cast<const typename V16<R>::type*>(spectra_dev);
       a.n_fil = n_fil;
       a.fchunk = n_fil;
-      a.t0 = t0;
       a.pp_kind = pp_kind;
-      a.l_eff = l_eff;
-      a.win_off = win_off;
-      a.seg_lo = seg_lo;
-      a.seg_hi = seg_hi;
+      a.t0 = t0e;
+      a.origin = origin;
+      a.seg_len = le;
+      a.k_lo = g_lo / le;
+      a.k_hi = (g_hi + le - 1) / le;
+      a.g_lo = g_lo;
+      a.g_hi = g_hi;
       a.pp_c = R(pp_c);
       a.out = static_cast<Cpx<R>*>(out);
       a.out_ld = out_ld;
       a.out_base = out_base;
+      a.dbg = debug_env();
       return launch_fused<R, decltype(lc)::value>(
           a, static_cast<cudaStream_t>(stream));
     });
   });
+}
+
+int olsb_fused_c2c(const void* x, int64_t x_base, int64_t n_s,
+                   const void* spectra_dev, int n_fil, int n, int m,
+                   int origin, int64_t l_eff, int t0, int64_t win_off,
+                   int64_t seg_lo, int64_t seg_hi, int pp_kind, double pp_c,
+                   void* out, int64_t out_ld, int64_t out_base,
+                   int precision, void* stream) {
+  if (n_s < 1 || n_fil < 0 || m < 1 || m > n || origin < 0 || origin >= m ||
+      seg_lo < 0 || seg_hi < seg_lo)
+    return OLSB_E_BAD_ARG;
+  if (l_eff < 1 || t0 < 0 || t0 + l_eff > n || win_off != origin - t0)
+    return OLSB_E_GEOMETRY;
+  // the reference segments [seg_lo, seg_hi) own outputs
+  // [seg_lo * l_eff, min(seg_hi * l_eff, n_s))
+  return fused_range(x, x_base, n_s, spectra_dev, n_fil, n, t0, origin, l_eff,
+                     seg_lo * l_eff, std::min<int64_t>(seg_hi * l_eff, n_s),
+                     pp_kind, pp_c, out, out_ld, out_base, precision, stream);
+}
+
+int olsb_fused_c2c_range(const void* x, int64_t x_base, int64_t n_s,
+                         const void* spectra_dev, int n_fil, int n, int m,
+                         int origin, int64_t g_lo, int64_t g_hi, int pp_kind,
+                         double pp_c, void* out, int64_t out_ld,
+                         int64_t out_base, int precision, void* stream) {
+  if (m < 1 || m > n || origin < 0 || origin >= m) return OLSB_E_BAD_ARG;
+  return fused_range(x, x_base, n_s, spectra_dev, n_fil, n, m - 1, origin,
+                     n - m + 1, g_lo, g_hi, pp_kind, pp_c, out, out_ld,
+                     out_base, precision, stream);
+}
+
+int olsb_input_extent(int n, int m, int origin, int64_t g_lo, int64_t g_hi,
+                      int64_t* x_lo, int64_t* x_hi) {
+  if (log2_of(n) < 0) return OLSB_E_BAD_LENGTH;
+  if (m < 1 || m > n || origin < 0 || origin >= m || g_hi < g_lo || !x_lo ||
+      !x_hi)
+    return OLSB_E_BAD_ARG;
+  int t0e;
+  long long le;
+  engine_grid(n, m - 1, n - m + 1, &t0e, &le);
+  const long long k_lo = g_lo / le, k_hi = (g_hi + le - 1) / le;
+  *x_lo = k_lo * le - t0e + origin;
+  *x_hi = (k_hi - 1) * le - t0e + origin + n;
+  return 0;
 }
 
 int olsb_copy2d_async(void* dst, int64_t dst_pitch_bytes, const void* src,

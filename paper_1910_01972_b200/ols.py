@@ -24,7 +24,6 @@ bit-identical results.
 from __future__ import annotations
 
 import math
-import time
 from dataclasses import dataclass
 from typing import Iterable, List, Optional, Tuple
 
@@ -350,13 +349,37 @@ def fused_launch(x: torch.Tensor, x_base: int, n_s: int,
               _stream_ptr() if stream is None else stream)
 
 
+def fused_range_launch(x: torch.Tensor, x_base: int, n_s: int,
+                       spec_dev: torch.Tensor, n_fil: int,
+                       seg_plan: SegmentPlan, g_lo: int, g_hi: int,
+                       pp: PostProcSpec, out: torch.Tensor, out_ld: int,
+                       out_base: int, precision: Precision,
+                       stream: Optional[int] = None) -> None:
+    """Outputs [g_lo, g_hi) through olsb_fused_c2c_range (shards, streams)."""
+    _lib.call("olsb_fused_c2c_range", x.data_ptr(), x_base, n_s,
+              spec_dev.data_ptr(), n_fil, seg_plan.fft_len, seg_plan.tap_len,
+              seg_plan.origin, g_lo, g_hi, pp.code, float(pp.scale),
+              out.data_ptr(), out_ld, out_base, precision.code,
+              _stream_ptr() if stream is None else stream)
+
+
+def input_extent(seg_plan: SegmentPlan, g_lo: int, g_hi: int) -> Tuple[int, int]:
+    """Input samples [x_lo, x_hi) the engine reads to produce outputs
+    [g_lo, g_hi) (its shard plus halos; clip to [0, n_s) before copying)."""
+    import ctypes
+    lo, hi = ctypes.c_int64(), ctypes.c_int64()
+    _lib.check(_lib.load().olsb_input_extent(
+        seg_plan.fft_len, seg_plan.tap_len, seg_plan.origin, g_lo, g_hi,
+        ctypes.byref(lo), ctypes.byref(hi)), "olsb_input_extent")
+    return lo.value, hi.value
+
+
 def _fused_streaming(signal, spec_dev, seg_plan, pp, precision, l_eff, t0,
                      win_off, n_seg, out, chunk_segments):
-    """Host-memory path: per chunk of segments, H2D of its input window,
-    fused kernel into a device staging tile, strided D2H into ``out``.
-    Three streams rotate over three staging slots so copies in both
-    directions overlap the kernel of the neighbouring chunks."""
-    n = seg_plan.fft_len
+    """Host-memory path: per chunk of outputs, H2D of its input extent, fused
+    kernel into a device staging tile, strided D2H into ``out``.  Three
+    streams rotate over three staging slots so copies in both directions
+    overlap the kernel of the neighbouring chunks."""
     n_s = signal.length
     n_fil = spec_dev.shape[0]
     x_host = signal.samples
@@ -365,37 +388,34 @@ def _fused_streaming(signal, spec_dev, seg_plan, pp, precision, l_eff, t0,
     if chunk_segments is None:
         # ~256 MiB of output per chunk
         chunk_segments = max(1, (256 << 20) // max(1, n_fil * l_eff * esize))
-    chunks = [(lo, min(lo + chunk_segments, n_seg))
-              for lo in range(0, n_seg, chunk_segments)]
+    w = max(32, (chunk_segments * l_eff) // 32 * 32)
+    chunks = [(g, min(g + w, n_s)) for g in range(0, n_s, w)]
     nslot = min(3, len(chunks))
-    w_max = chunk_segments * l_eff
-    x_len_max = w_max + n
+    ext = [input_extent(seg_plan, ga, gb) for ga, gb in chunks]
+    x_len_max = max(min(hi, n_s) - max(lo, 0) for lo, hi in ext)
     with torch.cuda.device(dev):
         streams = [torch.cuda.Stream() for _ in range(nslot)]
-        xbuf = [torch.empty(x_len_max, dtype=x_host.dtype, device=dev)
+        xbuf = [torch.empty(max(1, x_len_max), dtype=x_host.dtype, device=dev)
                 for _ in range(nslot)]
-        obuf = [torch.empty((n_fil, w_max), dtype=out.dtype, device=dev)
+        obuf = [torch.empty((n_fil, w), dtype=out.dtype, device=dev)
                 for _ in range(nslot)]
         ready = torch.cuda.current_stream()
         for s in streams:
             s.wait_stream(ready)
         lib = _lib.load()
-        for i, (lo, hi) in enumerate(chunks):
+        for i, ((ga, gb), (lo, hi)) in enumerate(zip(chunks, ext)):
             k = i % nslot
             st = streams[k]
-            g_lo = lo * l_eff
-            g_hi = min(hi * l_eff, n_s)
-            xa = max(0, g_lo + win_off)
-            xb = min(n_s, (hi - 1) * l_eff + win_off + n)
+            xa, xb = max(0, lo), min(n_s, hi)
             with torch.cuda.stream(st):
                 if xb > xa:
                     xbuf[k][:xb - xa].copy_(x_host[xa:xb], non_blocking=True)
-                fused_launch(xbuf[k], xa, n_s, spec_dev, n_fil, seg_plan,
-                             l_eff, t0, win_off, lo, hi, pp, obuf[k], w_max,
-                             g_lo, precision, st.cuda_stream)
+                fused_range_launch(xbuf[k], xa, n_s, spec_dev, n_fil, seg_plan,
+                                   ga, gb, pp, obuf[k], w, ga, precision,
+                                   st.cuda_stream)
                 _lib.check(lib.olsb_copy2d_async(
-                    out.data_ptr() + g_lo * esize, n_s * esize,
-                    obuf[k].data_ptr(), w_max * esize, (g_hi - g_lo) * esize,
+                    out.data_ptr() + ga * esize, n_s * esize,
+                    obuf[k].data_ptr(), w * esize, (gb - ga) * esize,
                     n_fil, 0, st.cuda_stream), "olsb_copy2d_async")
         for s in streams:
             ready.wait_stream(s)

@@ -28,17 +28,22 @@ static void run(const R* in, R* out, bool inverse) {
         else
           dif_pass_static<R, G::LOGE, G::G0>(x);
       } else {
-        Tw<R> tw[15];
+        struct Acc {
+          Tw<R> tw[15];
+          Tw<R> get0() const { return tw[0]; }
+          TwPair<R> get2(int p) const { return TwPair<R>{tw[2 * p - 1], tw[2 * p]}; }
+        } acc;
+        const int l = G::low_bits(q, t);
         for (int i = 0; i < 15; ++i) {
           double c, tt;
-          twiddle_entry(G::lo(q), i, G::low_bits(q, t), &c, &tt);
-          tw[i] = Tw<R>{R(c), R(tt)};
+          twiddle_entry(G::lo(q), i, l, G::tan01(q), &c, &tt);
+          acc.tw[i] = Tw<R>{R(c), R(tt)};
         }
-        auto acc = [&](int idx) { return tw[idx]; };
+        const int hb = G::lo(q) >= 2 ? (l >> (G::lo(q) - 2)) & 3 : 0;
         if (inverse)
-          dit_pass_rt<R>(x, acc);
+          dit_pass_rt<R, G::tan01(q)>(x, acc, hb);
         else
-          dif_pass_rt<R>(x, acc);
+          dif_pass_rt<R, G::tan01(q)>(x, acc, hb);
       }
       for (int e = 0; e < G::E; ++e) a[base + G::elem_part(q, e)] = x[e];
     }
@@ -81,9 +86,13 @@ int emu_fft_f(int logn, const float* in, float* out, int inverse) {
 int emu_fft_d(int logn, const double* in, double* out, int inverse) {
   return dispatch<double>(logn, in, out, inverse != 0);
 }
-// shared-memory layout / geometry probes for the layout tests
-int emu_pos(int dbl, int logn, int p) {
+// shared-memory layout probe for the layout tests: k1, p1, k2, p2, stride
+void emu_pad(int dbl, int logn, int* out5) {
   const Pad pd = pad_for(dbl != 0, logn);
-  return p + pd.p1 * (p >> pd.k1) + pd.p2 * (p >> pd.k2);
+  out5[0] = pd.k1;
+  out5[1] = pd.p1;
+  out5[2] = pd.k2;
+  out5[3] = pd.p2;
+  out5[4] = pd.stride;
 }
 }
