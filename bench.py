@@ -1,0 +1,371 @@
+"""Benchmark of the fused OLS engine (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1)
+
+Workload: BASELINE config 3, the FDAS-like filter bank named by north_star's
+70%-of-HBM target: 2^23 complex fp32 samples per GPU, 96 filters of 400
+taps, FFT segment N = 2048 (weak scaling: the global signal is N_gpus x 2^23
+samples, sharded contiguously with (M-1)-sample halos exchanged by NCCL
+send/recv inside every step).  A step = halo exchange + one fused-kernel
+launch producing every output of the rank's shard (filter spectra are
+precomputed and excluded, as in the reference bench, cli.py:229-233).
+Inputs: the reference generator convention (cli.py:41-55), synthetic.
+
+Prints ONE JSON line on rank 0.  ``value`` is device-resident throughput
+(output samples/s over all ranks, max-over-ranks device time), ``e2e`` the
+same metric through the public API from pinned host memory (H2D of the
+input, D2H of every output sample, copies overlapped with compute by the
+streaming path), ``roofline`` the fused kernel against the measured HBM
+bandwidth, ``cpu_baseline`` the oracle's C restatement of the reference on
+the host cores.  ``--impl reference`` times that CPU path alone.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+
+METRIC = ("convolved output samples/s (all filters) and HBM GB/s fraction at "
+          "1/2/4/8 B200")
+NS, M, NFIL, NFFT = 1 << 23, 400, 96, 2048
+WORKLOAD = ("cfg3 FDAS-like filter bank: 2^23 complex fp32 samples per GPU, "
+            "96 filters M=400, N=2048")
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clock / throttle sampling during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(sample_ns: int, repeats: int = 2):
+    """The oracle's C restatement of the reference fused path (fp32,
+    _kernels_nb.py:265-285), all host threads, on the first `sample_ns`
+    samples of the cfg3 workload with all 96 filters."""
+    import oracle
+    from cases import gen_inputs
+    x, taps = gen_inputs(NS, M, NFIL)
+    x = x[:sample_ns].astype(np.complex64)
+    taps = taps.astype(np.complex64)
+    threads = oracle.max_threads()
+    oracle.fused_convolve(x[:1 << 14], taps, NFFT, 0, "single", threads)
+    ts = []
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        oracle.fused_convolve(x, taps, NFFT, 0, "single", threads)
+        ts.append(time.perf_counter() - t0)
+    t = statistics.median(ts)
+    return {"value": sample_ns * NFIL / t, "unit": "samples/s",
+            "cores": threads, "kind": "port",
+            "sample": f"first {sample_ns} samples x {NFIL} filters of the "
+                      f"cfg3 signal, median of {repeats}",
+            "seconds": t}
+
+
+def run_reference(args, rank: int):
+    """--impl reference: the reference's CPU path (C port of its numba
+    kernels, oracle/) on the host cores, same metric and config."""
+    if rank != 0:
+        return
+    sample = 1 << 21
+    for _ in range(args.warmup):
+        cpu_baseline(sample, repeats=1)
+    vals = []
+    for _ in range(args.steps):
+        vals.append(cpu_baseline(sample, repeats=1))
+    v = statistics.median(r["value"] for r in vals)
+    secs = statistics.median(r["seconds"] for r in vals)
+    cb = dict(vals[0])
+    cb["value"] = v
+    cb.pop("seconds", None)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": secs * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "complex64 (fp32)",
+        "data": "synthetic (reference generator convention, cli.py:41-55)",
+        "config": {"workload": WORKLOAD, "sample_per_step": cb["sample"],
+                   "parallelism": "host threads (pthreads over segments)"},
+        "cpu_baseline": cb,
+        "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_1910_01972_b200 as ob
+    from paper_1910_01972_b200.ols import fused_range_launch
+    from paper_1910_01972_b200.sharding import exchange_halos, make_shards
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+
+    P = ob.Precision.single
+    ns_global = NS * world
+    p = ob.plan(ns_global, M, "c2c", 0, NFFT)
+    shards = make_shards(p, world)
+    me = shards[rank]
+    n_own = me.g_hi - me.g_lo
+
+    # ---- inputs (reference generator convention at N=1)
+    from cases import gen_inputs
+    if world == 1:
+        x_np, taps = gen_inputs(NS, M, NFIL)
+    else:
+        rng = np.random.default_rng([0, ns_global, M, NFIL, 0, rank + 1])
+        x_np = rng.standard_normal(n_own) + 1j * rng.standard_normal(n_own)
+        taps = (np.random.default_rng([0, ns_global, M, NFIL, 0, 0])
+                .standard_normal((NFIL, M)) * (1 + 1j))
+    own = torch.from_numpy(x_np[me.g_lo:me.g_hi] if world == 1 else x_np).to(
+        dev, torch.complex64)
+    fs = ob.transform_filters(ob.make_filterset(taps, 0, P, device=dev), p,
+                              "permuted")
+    out = torch.empty((NFIL, n_own), dtype=torch.complex64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step(ev=None):
+        xl = exchange_halos(own, shards, rank) if world > 1 else own
+        if ev is not None:
+            ev[0].record()
+        fused_range_launch(xl, me.x_lo if world > 1 else me.g_lo, ns_global,
+                           fs.spectra_dev, NFIL, p, me.g_lo, me.g_hi, ob.NONE,
+                           out, n_own, me.g_lo, P)
+        if ev is not None:
+            ev[1].record()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    kev = [(torch.cuda.Event(enable_timing=True),
+            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        for i in range(args.steps):
+            flush.zero_()          # L2 flush between timed steps (untimed)
+            starts[i].record()
+            step(kev[i])
+            ends[i].record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    step_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    kern_ms = [a.elapsed_time(b) for a, b in kev]
+    t = torch.tensor([step_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    step_ms_max = float(t.item())
+    ms_per_step = step_ms_max / args.steps
+    outputs_per_step = ns_global * NFIL
+    value = outputs_per_step / (ms_per_step * 1e-3)
+
+    hbm, peak_kind = peaks()
+    kmean = statistics.mean(kern_ms)
+    alg_bytes = 8 * n_own * (1 + NFIL)
+    achieved = alg_bytes / (kmean * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic_cfg3.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+
+    # ---- end to end through the public API from pinned host memory
+    e2e = None
+    if not args.no_e2e:
+        xh_lo, xh_hi = me.x_lo, me.x_hi
+        if world == 1:
+            xh = torch.from_numpy(x_np.astype(np.complex64)).pin_memory()
+            hsig = ob.make_signal(xh, "complex", P, device="cpu")
+            hout = torch.empty((NFIL, n_own), dtype=torch.complex64).pin_memory()
+            pe = ob.plan(NS, M, "c2c", 0, NFFT)
+            ob.convolve(hsig, fs, pe, out=hout)      # warm-up
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(args.e2e_steps):
+                ob.convolve(hsig, fs, pe, out=hout)
+            e1.record()
+            e1.synchronize()
+            e_ms = e0.elapsed_time(e1) / args.e2e_steps
+            h2d = xh.numel() * 8
+        else:
+            # every rank streams its own shard (owned samples + halos)
+            own_h = torch.empty(xh_hi - xh_lo, dtype=torch.complex64)
+            own_h[me.g_lo - xh_lo:me.g_hi - xh_lo] = own.cpu()
+            xl = exchange_halos(own, shards, rank).cpu()
+            own_h.copy_(xl)
+            xh = own_h.pin_memory()
+            hout = torch.empty((NFIL, n_own), dtype=torch.complex64).pin_memory()
+            from paper_1910_01972_b200.ols import _lib  # noqa: F401
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            xd = torch.empty_like(xh, device=dev)
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0.record()
+            for _ in range(args.e2e_steps):
+                xd.copy_(xh, non_blocking=True)
+                fused_range_launch(xd, xh_lo, ns_global, fs.spectra_dev, NFIL,
+                                   p, me.g_lo, me.g_hi, ob.NONE, out, n_own,
+                                   me.g_lo, P)
+                hout.copy_(out, non_blocking=True)
+            e1.record()
+            e1.synchronize()
+            e_ms = e0.elapsed_time(e1) / args.e2e_steps
+            h2d = xh.numel() * 8
+        te = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": outputs_per_step / (float(te.item()) * 1e-3),
+               "unit": "samples/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(NFIL * n_own * 8),
+               "ms_per_step": float(te.item()),
+               "path": "make_signal(pinned host) + convolve(out=pinned host)"
+                       " streaming chunks" if world == 1 else
+                       "per-rank H2D shard + fused_range + D2H"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_baseline(1 << 21)
+            cpu.pop("seconds", None)
+        except Exception as exc:  # the oracle needs gcc-built oracle/build
+            cpu = {"error": str(exc)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "samples/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "complex64 (fp32)",
+            "data": "synthetic (reference generator convention, cli.py:41-55)",
+            "config": {"workload": WORKLOAD, "signal_samples": ns_global,
+                       "filters": NFIL, "taps": M, "fft_len": NFFT,
+                       "parallelism": f"signal sharded over {world} GPU(s), "
+                                      "halo exchange by NCCL P2P",
+                       "l2": "flushed between timed steps (256 MiB memset)"},
+            "hbm_frac": achieved / hbm,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm,
+                         "unit": "GB/s", "frac": achieved / hbm,
+                         "traffic": traffic, "peak_source": peak_kind,
+                         "alg_bytes_per_launch": alg_bytes,
+                         "kernel_ms": kmean},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
