@@ -54,7 +54,7 @@ enum HMode : int {
 // barrier scope (0: CTA-wide __syncthreads, 1: named barrier per group),
 // MINB target CTAs per SM (register cap).
 template <class R_, int LOGN_, int SEGS_, int NBUF_, int HM_, int BAR_,
-          int MINB_>
+          int MINB_, int MIDREG_ = 0, int TMX_ = 0, int PREF_ = 0>
 struct KCfg {
   using R = R_;
   static constexpr int LOGN = LOGN_;
@@ -72,7 +72,31 @@ struct KCfg {
   // top-window twiddles live in registers (float: 30 registers) and its
   // table is built inside the exchange buffers, which it only occupies until
   // the registers are loaded
-  static constexpr bool TOPREG = !dbl && P >= 2;
+  // Tensor-memory residency (fused kernel, fp32, whole warpgroups): every
+  // thread parks per-thread state in its own TMEM lane instead of registers
+  //   TMX = 1: segment spectrum (32 words) + top-window twiddles (30 words)
+  //   TMX = 2: also the twiddles of the window below
+  // TMEM is read by tcgen05.ld at ~400 B/clk/SM, off the LSU pipe that
+  // carries the shared-memory exchanges (tools/mb_tmem.cu).
+  static constexpr int TMX =
+      (!dbl && P >= 2 && THREADS % 128 == 0) ? (P >= 3 ? TMX_ : (TMX_ ? 1 : 0))
+                                             : 0;
+  static constexpr int WG = THREADS / 128;     // warpgroups (TMEM lane sets)
+  static constexpr int CPW = 32 * (1 + TMX);   // TMEM columns per warpgroup
+  static constexpr int TCOLS = WG * CPW <= 32    ? 32
+                               : WG * CPW <= 64  ? 64
+                               : WG * CPW <= 128 ? 128
+                               : WG * CPW <= 256 ? 256
+                                                 : 512;
+  // H_TEX only: the next filter's spectrum is fetched into registers while
+  // the current one is transformed (hides the L2 latency of the fetch)
+  static constexpr bool PREF = PREF_ && HM_ == H_TEX && !dbl;
+  static constexpr bool TOPREG = !dbl && P >= 2 && !TMX;
+  // the top window's table is built in the exchange buffers (TOPREG / TMX)
+  static constexpr bool TOPOUT = TOPREG || TMX;
+  // the window below the top one keeps its twiddles in registers as well
+  // (fused kernel only): no shared-memory twiddle reads in the filter loop
+  static constexpr bool MIDREG = TOPREG && MIDREG_ && P >= 3;
   static constexpr size_t al(size_t b) { return (b + 127) & ~size_t(127); }
   static constexpr size_t buf_elems = size_t(SEGS) * L::stride;
   static constexpr size_t bufs_bytes =
@@ -81,10 +105,10 @@ struct KCfg {
   static constexpr size_t tab_bytes = al(size_t(G::tw_total()) * sizeof(Tw<R>));
   static constexpr size_t smem_bytes = tab_bytes + bufs_bytes;
   // ---- fused kernel: [bufs (+ top table at init) | low tables | H | bars]
-  static constexpr int lowtab_elems = TOPREG ? G::tw_offset(P - 1) : G::tw_total();
+  static constexpr int lowtab_elems = TOPOUT ? G::tw_offset(P - 1) : G::tw_total();
   static constexpr size_t f_bufs_bytes =
       P >= 2 ? std::max(bufs_bytes,
-                        TOPREG ? al(size_t(G::tw_entries(P - 1)) * sizeof(Tw<R>))
+                        TOPOUT ? al(size_t(G::tw_entries(P - 1)) * sizeof(Tw<R>))
                                : size_t(0))
              : 0;
   static constexpr size_t f_tab_off = f_bufs_bytes;
@@ -95,7 +119,8 @@ struct KCfg {
       HM == H_TMA ? 2 * h_bytes
                   : (HM == H_ASYNC ? al(size_t(THREADS) * VPT * 16) : 0);
   static constexpr size_t f_bar_off = f_h_off + f_h_bytes;
-  static constexpr size_t f_smem_bytes = f_bar_off + 16;
+  // [2 mbarriers | TMEM base address slot]
+  static constexpr size_t f_smem_bytes = f_bar_off + 32;
 };
 
 // configuration of the row kernels (filter spectra, standalone transforms)
@@ -235,6 +260,103 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
+// ---- tensor memory (tcgen05) as per-thread storage.  Thread i of warp w
+// owns TMEM lane 32 (w % 4) + i; `ta` = allocation base + lane + column.
+template <int COLS>
+__device__ __forceinline__ void tmem_alloc(uint32_t* slot) {
+  asm volatile(
+      "tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+          smem_u32(slot)),
+      "n"(COLS)
+      : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::
+                   : "memory");
+}
+template <int COLS>
+__device__ __forceinline__ void tmem_dealloc(uint32_t base) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base),
+               "n"(COLS)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// 32 consecutive columns of the thread's lane <-> 32 registers
+__device__ __forceinline__ void tmem_ld32(uint32_t ta, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,"
+      "%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,"
+      "%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]),
+        "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]),
+        "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+        "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
+        "=r"(r[30]), "=r"(r[31])
+      : "r"(ta));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_st32(uint32_t ta, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,"
+      "%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,"
+      "%27,%28,%29,%30,%31,%32};" ::"r"(ta),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]),
+      "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]),
+      "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]),
+      "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]),
+      "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]),
+      "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+// 16 complex<float> (a thread's segment) <-> 32 TMEM columns
+__device__ __forceinline__ void tmem_ld_cpx(uint32_t ta, Cpx<float>* v) {
+  uint32_t r[32];
+  tmem_ld32(ta, r);
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+    v[i] = Cpx<float>{__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])};
+}
+__device__ __forceinline__ void tmem_st_cpx(uint32_t ta, const Cpx<float>* v) {
+  uint32_t r[32];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    r[2 * i] = __float_as_uint(v[i].re);
+    r[2 * i + 1] = __float_as_uint(v[i].im);
+  }
+  tmem_st32(ta, r);
+}
+// a thread's 15 runtime twiddles of one window (30 columns, 2 spare)
+__device__ __forceinline__ void tmem_ld_tw(uint32_t ta, Tw<float>* w) {
+  uint32_t r[32];
+  tmem_ld32(ta, r);
+#pragma unroll
+  for (int i = 0; i < 15; ++i)
+    w[i] = Tw<float>{__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])};
+}
+__device__ __forceinline__ void tmem_st_tw(uint32_t ta, const Tw<float>* w) {
+  uint32_t r[32];
+#pragma unroll
+  for (int i = 0; i < 15; ++i) {
+    r[2 * i] = __float_as_uint(w[i].c);
+    r[2 * i + 1] = __float_as_uint(w[i].t);
+  }
+  r[30] = r[31] = 0u;
+  tmem_st32(ta, r);
+}
+// double-precision stubs (TMX is fp32-only; never instantiated for double)
+__device__ __forceinline__ void tmem_ld_cpx(uint32_t, Cpx<double>*) {}
+__device__ __forceinline__ void tmem_st_cpx(uint32_t, const Cpx<double>*) {}
+__device__ __forceinline__ void tmem_ld_tw(uint32_t, Tw<double>*) {}
+__device__ __forceinline__ void tmem_st_tw(uint32_t, const Tw<double>*) {}
+
 // predicated streaming store of one complex sample: stores iff o < span
 // (unsigned compare folds the o >= 0 test)
 __device__ __forceinline__ void st_cs_if(Cpx<float>* p, Cpx<float> v,
@@ -309,15 +431,19 @@ __device__ __forceinline__ void exchange(Cpx<typename C::R>* bufs, int& xc,
 }
 
 // full forward transform: x holds window P-1 on entry, window 0 (J) on exit.
-// With TOPREG the top window's 15 twiddles come from `twr`.
-template <class C, bool TOPREG, class H = NoHook, class H2 = NoHook>
+// With TOPREG the top window's 15 twiddles come from `twr`, with MIDREG the
+// next window's from `twm`; with TMX they are read from TMEM at `tb`.
+template <class C, bool TOPREG, bool MIDREG = false, class H = NoHook,
+          class H2 = NoHook>
 __device__ __forceinline__ void forward_fft(Cpx<typename C::R>* x,
                                             const Tw<typename C::R>* lowtab,
                                             const Tw<typename C::R>* twr,
+                                            const Tw<typename C::R>* twm,
                                             Cpx<typename C::R>* bufs, int& xc,
                                             int sl, int t,
                                             const H& last_hook = H{},
-                                            const H2& post_hook = H2{}) {
+                                            const H2& post_hook = H2{},
+                                            uint32_t tb = 0) {
   using R = typename C::R;
   using G = typename C::G;
   constexpr int LOGN = C::LOGN;
@@ -331,8 +457,14 @@ __device__ __forceinline__ void forward_fft(Cpx<typename C::R>* x,
     if constexpr (q == 0) {
       dif_pass_static<R, C::LOGE, G::G0>(x);
     } else {
-      if constexpr (q == G::P - 1 && TOPREG) {
+      if constexpr (C::TMX && (q == G::P - 1 || (q == G::P - 2 && C::TMX == 2))) {
+        Tw<R> tw[16];
+        tmem_ld_tw(tb + (q == G::P - 1 ? 32u : 64u), tw);
+        dif_pass_rt<R, G::tan01(q)>(x, TwRegs<R>{tw}, top_bits<LOGN, q>(t));
+      } else if constexpr (q == G::P - 1 && TOPREG) {
         dif_pass_rt<R, G::tan01(q)>(x, TwRegs<R>{twr}, top_bits<LOGN, q>(t));
+      } else if constexpr (q == G::P - 2 && MIDREG) {
+        dif_pass_rt<R, G::tan01(q)>(x, TwRegs<R>{twm}, top_bits<LOGN, q>(t));
       } else {
         dif_pass_rt<R, G::tan01(q)>(
             x, tw_smem<R, LOGN, q>(lowtab + G::tw_offset(q), t),
@@ -376,6 +508,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   Tw<R>* lowtab = reinterpret_cast<Tw<R>*>(smem_raw + C::f_tab_off);
   Cpx<R>* hbuf = reinterpret_cast<Cpx<R>*>(smem_raw + C::f_h_off);
   uint64_t* hbar = reinterpret_cast<uint64_t*>(smem_raw + C::f_bar_off);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem_raw + C::f_bar_off + 16);
 
   const int tid = threadIdx.x;
   const int sl = tid / T;
@@ -394,13 +527,37 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
       fence_proxy_async();
     }
   }
+  if constexpr (C::TMX) {
+    if (tid < 32) tmem_alloc<C::TCOLS>(tslot);
+    tmem_fence_before();
+  }
   build_tables<R, LOGN>(lowtab,
-                        C::TOPREG ? reinterpret_cast<Tw<R>*>(bufs) : nullptr);
+                        C::TOPOUT ? reinterpret_cast<Tw<R>*>(bufs) : nullptr);
   __syncthreads();
+  uint32_t tbase = 0, tb = 0;
+  if constexpr (C::TMX) {
+    tmem_fence_after();
+    tbase = *tslot;
+    const int w = tid / 32;
+    tb = tbase + (uint32_t((w & 3) * 32) << 16) + uint32_t((w >> 2) * C::CPW);
+  }
 
   // top-window twiddles: fixed per thread for the kernel lifetime
   Tw<R> twr[15];
-  if constexpr (C::TOPREG) {
+  Tw<R> twm[15];
+  if constexpr (C::MIDREG || C::TMX == 2) {
+    constexpr int q = P - 2;
+    const TwSmem<R> tt = tw_smem<R, LOGN, q>(lowtab + G::tw_offset(q), t);
+    twm[0] = tt.get0();
+#pragma unroll
+    for (int pp = 1; pp < 8; ++pp) {
+      const TwPair<R> w = tt.get2(pp);
+      twm[2 * pp - 1] = w.a;
+      twm[2 * pp] = w.b;
+    }
+    if constexpr (C::TMX == 2) tmem_st_tw(tb + 64, twm);
+  }
+  if constexpr (C::TOPOUT) {
     constexpr int q = P - 1;
     const TwSmem<R> tt =
         tw_smem<R, LOGN, q>(reinterpret_cast<const Tw<R>*>(bufs), t);
@@ -410,6 +567,10 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
       const TwPair<R> w = tt.get2(pp);
       twr[2 * pp - 1] = w.a;
       twr[2 * pp] = w.b;
+    }
+    if constexpr (C::TMX) {
+      tmem_st_tw(tb + 32, twr);
+      tmem_wait_st();
     }
     __syncthreads();  // the exchange buffers are free from here on
   }
@@ -435,10 +596,22 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
       cp_async_commit();
     }
   };
+  // PREF: this thread's VPT vectors of the next filter, in registers
+  float4 hn[C::PREF ? C::VPT : 1];
+  auto fetch = [&](int f) {
+    if constexpr (C::PREF) {
+      const int hb = f * (C::VPT * T) + t;
+      sfor<0, C::VPT>([&](auto uc) {
+        constexpr int u = decltype(uc)::value;
+        hn[u] = tex1Dfetch<float4>(a.htex, hb + u * T);
+      });
+    }
+  };
   if (blockIdx.x < nitems) {
     const int f0 = int(blockIdx.x % nfch) * a.fchunk;
     if (C::HM == H_TMA && tid == 0) issue(f0, 0);
     prefetch(f0);
+    fetch(f0);
   }
 
   const R inv_n = R(1) / R(G::N);
@@ -480,19 +653,25 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
       });
     }
     // ---- forward FFT (dif_fwd, _kernels_nb.py:11-28); the spectrum stays in
-    // registers with the inverse's 1/N and the scale post-process folded in.
-    // H_TMA: thread 0 makes sure this item's first spectrum has landed before
-    // the forward FFT's last barrier; everybody else learns it from the barrier
+    // registers (or TMEM) with the inverse's 1/N and the scale post-process
+    // folded in.  H_TMA: thread 0 makes sure this item's first spectrum has
+    // landed before the forward FFT's last barrier; everybody else learns it
+    // from the barrier
     auto wait_cur = [&]() {
       if constexpr (C::HM == H_TMA && P > 1) {
         if (tid == 0) mbar_wait(&hbar[hseq & 1u], (hseq >> 1) & 1u);
       }
     };
-    forward_fft<C, C::TOPREG>(x, lowtab, twr, bufs, xc, sl, t, wait_cur);
+    forward_fft<C, C::TOPREG, C::MIDREG>(x, lowtab, twr, twm, bufs, xc, sl, t,
+                                         wait_cur, NoHook{}, tb);
     {
       const R sc = a.pp_kind == OLSB_PP_SCALE ? inv_n * a.pp_c : inv_n;
 #pragma unroll
       for (int e = 0; e < E; ++e) x[e] = cscale(x[e], sc);
+    }
+    if constexpr (C::TMX) {
+      tmem_st_cpx(tb, x);
+      tmem_wait_st();
     }
 
     for (int f = f_lo; f < f_hi; ++f, ++hseq) {
@@ -508,11 +687,19 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
       // ---- pointwise multiply, both operands bit-reversed
       // (_kernels_nb.py:280-282)
       Cpx<R> y[E];
+      if constexpr (C::TMX) tmem_ld_cpx(tb, y);  // y = segment spectrum
+      const Cpx<R>* xs = C::TMX ? y : x;
       auto mulh = [&](int u, float4 h) {
-        y[2 * u] = cmul(x[2 * u], Cpx<R>{R(h.x), R(h.y)});
-        y[2 * u + 1] = cmul(x[2 * u + 1], Cpx<R>{R(h.z), R(h.w)});
+        y[2 * u] = cmul(xs[2 * u], Cpx<R>{R(h.x), R(h.y)});
+        y[2 * u + 1] = cmul(xs[2 * u + 1], Cpx<R>{R(h.z), R(h.w)});
       };
-      if constexpr (C::HM == H_TMA) {
+      if constexpr (C::PREF) {
+        sfor<0, C::VPT>([&](auto uc) {
+          constexpr int u = decltype(uc)::value;
+          mulh(u, hn[u]);
+        });
+        if (f_next >= 0) fetch(f_next);
+      } else if constexpr (C::HM == H_TMA) {
         const float4* hs =
             reinterpret_cast<const float4*>(hbuf + size_t(slot) * G::N) + t;
         sfor<0, C::VPT>([&](auto uc) {
@@ -559,8 +746,14 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
         } else {
           exchange<C, q - 1, q>(bufs, xc, sl, t, y);
         }
-        if constexpr (q == P - 1 && C::TOPREG) {
+        if constexpr (C::TMX && (q == P - 1 || (q == P - 2 && C::TMX == 2))) {
+          Tw<R> tw[16];
+          tmem_ld_tw(tb + (q == P - 1 ? 32u : 64u), tw);
+          dit_pass_rt<R, G::tan01(q)>(y, TwRegs<R>{tw}, top_bits<LOGN, q>(t));
+        } else if constexpr (q == P - 1 && C::TOPREG) {
           dit_pass_rt<R, G::tan01(q)>(y, TwRegs<R>{twr}, top_bits<LOGN, q>(t));
+        } else if constexpr (q == P - 2 && C::MIDREG) {
+          dit_pass_rt<R, G::tan01(q)>(y, TwRegs<R>{twm}, top_bits<LOGN, q>(t));
         } else {
           dit_pass_rt<R, G::tan01(q)>(
               y, tw_smem<R, LOGN, q>(lowtab + G::tw_offset(q), t),
@@ -584,6 +777,11 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
         });
       }
     }
+  }
+  if constexpr (C::TMX) {
+    tmem_fence_before();
+    __syncthreads();
+    if (tid < 32) tmem_dealloc<C::TCOLS>(tbase);
   }
 }
 
@@ -630,7 +828,7 @@ __global__ void __launch_bounds__(C::THREADS)
     }
     // every load of the group precedes any store (in-place safety)
     __syncthreads();
-    forward_fft<C, false>(x, tab, nullptr, bufs, xc, sl, t);
+    forward_fft<C, false>(x, tab, nullptr, nullptr, bufs, xc, sl, t);
     if (live) {
       if (a.out_perm) {
         Cpx<R>* o = a.out_perm + size_t(r) * G::N + G::thread_part(0, t);

@@ -81,9 +81,25 @@ struct Geo {
   // runtime twiddle entries of window q: 8 pair slots (16 entries, one
   // unused) per low-bit value l, see twiddle_slot()
   static constexpr int tw_entries(int q) { return q == 0 ? 0 : 16 << lo(q); }
-  // windows whose first two stages use the FMA (tangent) forms: the top
-  // window when lanes hold l's low 5 bits and its top 2 bits are warp bits
-  static constexpr bool tan01(int q) { return q == P - 1 && lo(q) >= 7; }
+  // Thread-bit remap of window q: its low bits l = p & (2^lo - 1) pick the
+  // tangent form of stages 0-1 through their top two bits ("hb", index bits
+  // lo-2 and lo-1).  Those must be warp bits for the choice to be uniform.
+  // With the plain mapping (thread bit i -> index bit i for i < lo) that
+  // holds iff lo >= 7; a lower window with at least two warp bits to spare
+  // swaps thread bits (lo-2, lo-1) with the top two thread bits instead.
+  static constexpr bool remap(int q) {
+    return q >= 1 && lo(q) >= 2 && lo(q) < 7 && LOGT >= 7 && lo(q) <= LOGT - 2;
+  }
+  // windows whose first two stages use the FMA (tangent) forms
+  static constexpr bool tan01(int q) {
+    return q >= 1 && (lo(q) >= 7 || remap(q));
+  }
+  static OLSB_HD int perm(int q, int t) {
+    if (!remap(q)) return t;
+    const int a = remap(q) ? lo(q) - 2 : 0, b = remap(q) ? LOGT - 2 : 0;
+    const int x = ((t >> a) ^ (t >> b)) & 3;  // swap two 2-bit fields
+    return t ^ (x << a) ^ (x << b);
+  }
   static constexpr int tw_offset(int q) {
     int off = 0;
     for (int i = 1; i < q; ++i) off += tw_entries(i);
@@ -94,37 +110,42 @@ struct Geo {
   // bit fields, so p = thread_part + elem_part)
   static OLSB_HD int thread_part(int q, int t) {
     const int l = lo(q);
-    return ((t >> l) << (l + LOGE)) | (t & ((1 << l) - 1));
+    const int u = perm(q, t);
+    return ((u >> l) << (l + LOGE)) | (u & ((1 << l) - 1));
   }
   static constexpr int elem_part(int q, int e) { return e << lo(q); }
-  static OLSB_HD int low_bits(int q, int t) { return t & ((1 << lo(q)) - 1); }
+  static OLSB_HD int low_bits(int q, int t) {
+    return perm(q, t) & ((1 << lo(q)) - 1);
+  }
 };
 
 // ---------------------------------------------------------------------------
-// shared-memory exchange layout: pos(p) = p + P1*(p>>K1) + P2*(p>>K2).
+// shared-memory exchange layout: pos(p) = p + P1*(p>>K1) + P2*(p>>K2) +
+// P3*(p>>K3).
 // Linear over disjoint bit fields, so every address is a per-thread base plus
 // a compile-time immediate.  Parameters found by tools/smem_layout_search.py
 // (zero bank conflicts for every access of both transforms).
 // ---------------------------------------------------------------------------
 struct Pad {
-  int k1, p1, k2, p2, stride;
+  int k1, p1, k2, p2, k3, p3, stride;
 };
 
 constexpr Pad pad_for(bool dbl, int logn) {
-  constexpr Pad f[13] = {{2, 0, 2, 0, 2},    {2, 0, 2, 0, 2},
-                         {2, 0, 2, 0, 6},    {2, 0, 2, 0, 10},
-                         {2, 0, 2, 0, 18},   {2, 0, 4, 8, 42},
-                         {4, 2, 5, 4, 76},   {2, 0, 4, 2, 152},
-                         {2, 0, 4, 2, 286},  {4, 2, 7, 2, 580},
-                         {4, 2, 7, 4, 1178}, {4, 2, 7, 8, 2422},
-                         {2, 0, 4, 2, 4606}};
-  constexpr Pad d[13] = {{2, 0, 2, 0, 1},    {2, 0, 2, 0, 1},
-                         {2, 0, 2, 0, 5},    {2, 0, 2, 0, 9},
-                         {2, 0, 2, 0, 17},   {2, 0, 4, 1, 34},
-                         {2, 0, 4, 1, 68},   {2, 0, 4, 1, 135},
-                         {2, 0, 4, 1, 271},  {2, 0, 4, 1, 543},
-                         {2, 0, 4, 1, 1087}, {2, 0, 4, 1, 2175},
-                         {2, 0, 4, 1, 4351}};
+  // LOGN 11 / 12 carry the Geo::remap thread-bit swap of the middle window
+  constexpr Pad f[13] = {{2, 0, 2, 0, 2, 0, 2},    {2, 0, 2, 0, 2, 0, 2},
+                         {2, 0, 2, 0, 2, 0, 6},    {2, 0, 2, 0, 2, 0, 10},
+                         {2, 0, 2, 0, 2, 0, 18},   {2, 0, 4, 8, 4, 0, 42},
+                         {4, 2, 5, 4, 5, 0, 76},   {2, 0, 4, 2, 4, 0, 152},
+                         {2, 0, 4, 2, 4, 0, 286},  {4, 2, 7, 2, 7, 0, 580},
+                         {4, 2, 7, 4, 7, 0, 1178}, {4, 2, 7, 2, 10, 4, 2336},
+                         {4, 2, 10, 4, 10, 0, 4618}};
+  constexpr Pad d[13] = {{2, 0, 2, 0, 2, 0, 1},    {2, 0, 2, 0, 2, 0, 1},
+                         {2, 0, 2, 0, 2, 0, 5},    {2, 0, 2, 0, 2, 0, 9},
+                         {2, 0, 2, 0, 2, 0, 17},   {2, 0, 4, 1, 4, 0, 34},
+                         {2, 0, 4, 1, 4, 0, 68},   {2, 0, 4, 1, 4, 0, 135},
+                         {2, 0, 4, 1, 4, 0, 271},  {2, 0, 4, 1, 4, 0, 543},
+                         {2, 0, 4, 1, 4, 0, 1087}, {4, 1, 9, 2, 9, 0, 2181},
+                         {4, 1, 10, 4, 10, 0, 4363}};
   return dbl ? d[logn] : f[logn];
 }
 
@@ -132,7 +153,8 @@ template <class R, int LOGN>
 struct SmemLayout {
   static constexpr Pad pd = pad_for(std::is_same<R, double>::value, LOGN);
   static OLSB_HD constexpr int pos(int p) {
-    return p + pd.p1 * (p >> pd.k1) + pd.p2 * (p >> pd.k2);
+    return p + pd.p1 * (p >> pd.k1) + pd.p2 * (p >> pd.k2) +
+           pd.p3 * (p >> pd.k3);
   }
   static constexpr int stride = pd.stride;  // per segment, in Cpx<R> units
 };

@@ -94,25 +94,32 @@ template <class R, int LOGN>
 struct DefaultPolicy {
   static constexpr bool dbl = std::is_same<R, double>::value;
   static constexpr int T = Geo<LOGN>::T;
-  // fp32: one 128-thread group of segments per CTA, one exchange buffer,
-  // spectra through the TEX path, 16 warps per SM
+  // fp32 (OLSB_VARIANT=2 / 3 of the sweep in DESIGN.md §5): 128-thread CTAs,
+  // 4 CTAs per SM, segment spectrum and runtime-window twiddles in TMEM, the
+  // next filter's spectrum prefetched through the TEX path; N = 4096 double
+  // buffers the exchange (one barrier per exchange).
   static constexpr int SEGS = dbl ? std::max(1, 256 / T) : std::max(1, 128 / T);
-  using type = KCfg<R, LOGN, SEGS, 1, dbl ? H_LDG : H_TEX, 0,
-                    dbl ? 1 : std::max(1, 512 / (SEGS * T))>;
+  using type = KCfg<R, LOGN, SEGS, (!dbl && LOGN == 12) ? 2 : 1,
+                    dbl ? H_LDG : H_TEX, 0,
+                    dbl ? 1 : std::max(1, 512 / (SEGS * T)), 0, dbl ? 0 : 2,
+                    dbl ? 0 : 1>;
 };
 
-// tuning variants for fp32 N >= 2048 (OLSB_VARIANT)
+// tuning variants for fp32 (OLSB_VARIANT).  A CTA holds SEGS x max(1,
+// 128 / T) segments; MINB is CTAs per SM for a 128-thread CTA.
 template <int LOGN, int V>
 struct Variant {
   static constexpr int T = Geo<LOGN>::T;
-  // {SEGS, NBUF, HM, BAR, MINB (CTAs/SM at T = 128)}
-  static constexpr int tab[8][5] = {
-      {1, 1, H_TEX, 0, 4}, {1, 2, H_TEX, 0, 4}, {2, 2, H_TEX, 1, 2},
-      {1, 1, H_TMA, 0, 4}, {1, 2, H_LDG, 0, 4}, {2, 1, H_TEX, 0, 2},
-      {2, 2, H_TMA, 0, 2}, {1, 1, H_LDG, 0, 4}};
-  static constexpr int segs = tab[V][0];
-  static constexpr int minb = std::max(1, tab[V][4] * 128 / T);
-  using type = KCfg<float, LOGN, segs, tab[V][1], tab[V][2], tab[V][3], minb>;
+  // {SEGS, NBUF, HM, BAR, MINB, MIDREG, TMX, PREF}
+  static constexpr int tab[8][8] = {
+      {1, 1, H_TEX, 0, 4, 0, 0, 0}, {1, 1, H_TEX, 0, 4, 0, 1, 1},
+      {1, 1, H_TEX, 0, 4, 0, 2, 1}, {1, 2, H_TEX, 0, 4, 0, 2, 1},
+      {1, 1, H_TEX, 0, 5, 0, 1, 0}, {1, 2, H_TEX, 0, 4, 0, 1, 1},
+      {2, 1, H_TEX, 1, 2, 0, 2, 1}, {1, 1, H_TEX, 0, 8, 0, 1, 0}};
+  static constexpr int segs = tab[V][0] * std::max(1, 128 / T);
+  static constexpr int minb = std::max(1, tab[V][4] * 128 / (segs * T));
+  using type = KCfg<float, LOGN, segs, tab[V][1], tab[V][2], tab[V][3], minb,
+                    tab[V][5], tab[V][6], tab[V][7]>;
 };
 
 inline int debug_env() {
@@ -137,6 +144,9 @@ int launch_fused_cfg(FusedArgs<typename C::R> a, cudaStream_t st) {
   int resident = 0;
   int rc = prepare(kern, C::f_smem_bytes, C::THREADS, &resident);
   if (rc) return rc;
+  // the occupancy API reports one CTA per SM for kernels that allocate
+  // tensor memory; the TMEM policies size their columns for MINB CTAs/SM
+  if constexpr (C::TMX) resident = std::max(resident, C::MINB * num_sms());
   if constexpr (C::HM == H_TEX) {
     rc = spectra_texture(a.spec, size_t(a.n_fil) * C::VPT * C::T * 16, &a.htex);
     if (rc) return rc;
@@ -154,7 +164,7 @@ int launch_fused_cfg(FusedArgs<typename C::R> a, cudaStream_t st) {
 
 template <class R, int LOGN>
 int launch_fused(FusedArgs<R> a, cudaStream_t st) {
-  if constexpr (std::is_same<R, float>::value && LOGN >= 11) {
+  if constexpr (std::is_same<R, float>::value) {
     switch (variant_env()) {
       case 0: return launch_fused_cfg<typename Variant<LOGN, 0>::type>(a, st);
       case 1: return launch_fused_cfg<typename Variant<LOGN, 1>::type>(a, st);

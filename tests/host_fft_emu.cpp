@@ -86,13 +86,16 @@ int emu_fft_f(int logn, const float* in, float* out, int inverse) {
 int emu_fft_d(int logn, const double* in, double* out, int inverse) {
   return dispatch<double>(logn, in, out, inverse != 0);
 }
-// shared-memory layout probe for the layout tests: k1, p1, k2, p2, stride
-void emu_pad(int dbl, int logn, int* out5) {
+// shared-memory layout probe for the layout tests:
+// k1, p1, k2, p2, k3, p3, stride
+void emu_pad(int dbl, int logn, int* out7) {
   const Pad pd = pad_for(dbl != 0, logn);
-  out5[0] = pd.k1;
-  out5[1] = pd.p1;
-  out5[2] = pd.k2;
-  out5[3] = pd.p2;
-  out5[4] = pd.stride;
+  out7[0] = pd.k1;
+  out7[1] = pd.p1;
+  out7[2] = pd.k2;
+  out7[3] = pd.p2;
+  out7[4] = pd.k3;
+  out7[5] = pd.p3;
+  out7[6] = pd.stride;
 }
 }

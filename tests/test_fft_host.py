@@ -79,13 +79,12 @@ def test_smem_layout_conflict_free_and_injective(emu, dbl, logn):
     padded map is injective (kernel CTA = 256 threads = 256/T segments)."""
     sys.path.insert(0, os.path.join(ROOT, "tools"))
     import smem_layout_search as S
-    pd = (ctypes.c_int * 5)()
+    pd = (ctypes.c_int * 7)()
     emu.emu_pad(dbl, logn, pd)
-    k1, p1, k2, p2, stride = list(pd)
+    *kp, stride = list(pd)
     n = 1 << logn
-    pos = [S.pos(p, k1, p1, k2, p2) for p in range(n)]
+    pos = [S.pos(p, *kp) for p in range(n)]
     assert len(set(pos)) == n and max(pos) < stride
     loge, logt, _, _, _ = S.geo(logn)
     segs = max(1, 256 >> logt)
-    assert S.conflict_free(logn, min(segs, 64), k1, p1, k2, p2, stride,
-                           bool(dbl))
+    assert S.conflict_free(logn, min(segs, 64), *kp, stride, bool(dbl))

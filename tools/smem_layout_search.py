@@ -29,17 +29,32 @@ def geo(logn):
     return loge, logt, p, g0, los
 
 
+def perm(logn, q, t):
+    """Geo::perm (olsb_fft.cuh): lower windows swap thread bits (lo-2, lo-1)
+    with the top two thread bits so the tangent-form choice is warp-uniform."""
+    loge, logt, p, g0, los = geo(logn)
+    lo = los[q]
+    if not (q >= 1 and 2 <= lo < 7 and logt >= 7 and lo <= logt - 2):
+        return t
+    a, b = lo - 2, logt - 2
+    x = ((t >> a) ^ (t >> b)) & 3
+    return t ^ (x << a) ^ (x << b)
+
+
 def index(logn, q, e, t):
     loge, logt, p, g0, los = geo(logn)
     lo = los[q]
+    t = perm(logn, q, t)
     return ((t >> lo) << (lo + loge)) | (e << lo) | (t & ((1 << lo) - 1))
 
 
-def pos(p, k1, p1, k2, p2):
-    return p + p1 * (p >> k1) + p2 * (p >> k2)
+def pos(p, *kp):
+    """pos(p, k1, p1, k2, p2[, k3, p3]) = p + sum_i p_i * (p >> k_i)."""
+    return p + sum(kp[i + 1] * (p >> kp[i]) for i in range(0, len(kp), 2))
 
 
-def conflict_free(logn, segs, k1, p1, k2, p2, stride, dbl):
+def conflict_free(logn, segs, *args):
+    *kp, stride, dbl = args
     loge, logt, npass, g0, los = geo(logn)
     T = 1 << logt
     E = 1 << loge
@@ -61,7 +76,7 @@ def conflict_free(logn, segs, k1, p1, k2, p2, stride, dbl):
                             continue
                         seg, t = divmod(tid, T)
                         pp = index(logn, q, e0, t)
-                        a = seg * stride + pos(pp, k1, p1, k2, p2)
+                        a = seg * stride + pos(pp, *kp)
                         if width_elems == 2:
                             if a % 2:
                                 return False
@@ -76,30 +91,29 @@ def conflict_free(logn, segs, k1, p1, k2, p2, stride, dbl):
     return True
 
 
-def span(logn, k1, p1, k2, p2):
+def span(logn, *kp):
     n = 1 << logn
-    return pos(n - 1, k1, p1, k2, p2) + 1
+    return pos(n - 1, *kp) + 1
 
 
-def search(logn, segs, dbl):
+def search(logn, segs, dbl, nterms=2):
+    """Cheapest nterms-term padding (3 terms needed where Geo::remap swaps
+    thread bits, e.g. fp32 LOGN = 11)."""
     best = None
     ks = list(range(2, logn + 1))
-    pads = [0, 1, 2, 4, 8, 16]
-    for k1, k2 in itertools.product(ks, ks):
-        if k2 < k1:
-            continue
-        for p1, p2 in itertools.product(pads, pads):
-            if k1 == k2 and p2:
-                continue
-            sp = span(logn, k1, p1, k2, p2)
+    pads = [0, 1, 2, 3, 4, 6, 8, 12, 16]
+    for K in itertools.combinations_with_replacement(ks, nterms):
+        for P in itertools.product(pads, repeat=nterms):
+            kp = [v for pair in zip(K, P) for v in pair]
+            sp = span(logn, *kp)
             for extra in range(0, 17, 1 if segs > 1 else 17):
                 stride = sp + extra
                 if dbl is False and stride % 2:
-                    continue
-                if conflict_free(logn, segs, k1, p1, k2, p2, stride, dbl):
-                    cost = stride * segs
-                    if best is None or cost < best[0]:
-                        best = (cost, k1, p1, k2, p2, stride)
+                    stride += 1
+                if best is not None and stride * segs >= best[0]:
+                    break
+                if conflict_free(logn, segs, *kp, stride, dbl):
+                    best = (stride * segs, *kp, stride)
                     break
     return best
 
@@ -111,11 +125,13 @@ if __name__ == "__main__":
             loge, logt, _, _, _ = geo(logn)
             T = 1 << logt
             segs = max(1, 128 // T) if not dbl else max(1, 64 // T)
-            b = search(logn, segs, dbl)
+            b = search(logn, segs, dbl) or search(logn, segs, dbl, 3)
             n = 1 << logn
             print(f"{'double' if dbl else 'float '} LOGN={logn:2d} segs={segs:3d} "
                   f"-> {b}  overhead {b[0] / (n * segs) - 1:.3f}", file=sys.stderr)
             out.append((dbl, logn, segs, b))
     for dbl, logn, segs, b in out:
-        cost, k1, p1, k2, p2, stride = b
-        print(f"  {{{int(dbl)}, {logn}, {segs}, {k1}, {p1}, {k2}, {p2}, {stride}}},")
+        kp = list(b[1:-1])
+        while len(kp) < 6:
+            kp += [kp[-2], 0]
+        print(f"  {{{int(dbl)}, {logn}, {segs}, {', '.join(map(str, kp))}, {b[-1]}}},")
