@@ -3,7 +3,9 @@
     python -m paper_1910_01972_b200.build [--verbose]
 
 The library is a plain C-ABI shared object (include/olsb.h) loaded with
-ctypes; no torch headers are involved, so it builds in seconds and travels to
+ctypes; no torch headers are involved.  The kernel instantiations of each FFT
+length are a separate object (olsb_inst.cu, -DOLSB_LOGN=L) compiled in
+parallel, then linked with the C ABI (olsb_kernels.cu).  The .so travels to
 the GPU box inside the repo snapshot.
 """
 
@@ -14,19 +16,25 @@ import os
 import shutil
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libolsb.so")
-SOURCES = [os.path.join(CSRC, "olsb_kernels.cu")]
-HEADERS = [os.path.join(CSRC, "olsb_fft.cuh"), os.path.join(INCLUDE, "olsb.h")]
+SOURCES = [os.path.join(CSRC, "olsb_kernels.cu"),
+           os.path.join(CSRC, "olsb_inst.cu")]
+HEADERS = [os.path.join(CSRC, h) for h in
+           ("olsb_fft.cuh", "olsb_engine.cuh", "olsb_launch.cuh")] + [
+    os.path.join(INCLUDE, "olsb.h")]
+LOGNS = range(2, 13)
+OBJDIR = os.path.join(PKG, "build_obj")
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
 ]
 
 
@@ -44,19 +52,35 @@ def needs_build() -> bool:
     return any(os.path.getmtime(s) > t for s in SOURCES + HEADERS)
 
 
+def _run(cmd, verbose):
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+        raise RuntimeError("nvcc failed building libolsb.so")
+    return res.stderr if verbose else ""
+
+
 def build(verbose: bool = False, force: bool = False) -> str:
     if not force and not needs_build():
         return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC]
+    os.makedirs(OBJDIR, exist_ok=True)
+    base = [nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC]
     if verbose:
-        cmd += ["-Xptxas", "-v"]
-    cmd += [*SOURCES, "-o", LIB + ".tmp", "-lcudart"]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libolsb.so")
+        base += ["-Xptxas", "-v"]
+    jobs = [(base + ["-c", SOURCES[0], "-o",
+                     os.path.join(OBJDIR, "olsb_kernels.o")])]
+    for lg in LOGNS:
+        jobs.append(base + [f"-DOLSB_LOGN={lg}", "-c", SOURCES[1], "-o",
+                            os.path.join(OBJDIR, f"olsb_inst_{lg}.o")])
+    # longest (largest N) first
+    jobs = [jobs[0]] + jobs[1:][::-1]
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        logs = list(ex.map(lambda c: _run(c, verbose), jobs))
+    objs = [j[-1] for j in jobs]
+    _run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+          *objs, "-o", LIB + ".tmp", "-lcudart"], False)
     if verbose:
-        sys.stderr.write(res.stderr)
+        sys.stderr.write("".join(logs))
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

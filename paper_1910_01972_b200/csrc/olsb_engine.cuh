@@ -367,6 +367,27 @@ __device__ __forceinline__ void st_cs_if(Cpx<float>* p, Cpx<float> v,
       "f"(v.re), "f"(v.im), "r"(o), "r"(span)
       : "memory");
 }
+// streaming store of one complex sample iff (mask & bit)
+template <unsigned BIT>
+__device__ __forceinline__ void st_cs_mask(Cpx<float>* p, Cpx<float> v,
+                                           unsigned mask) {
+  asm volatile(
+      "{\n .reg .pred q;\n .reg .b32 m;\n and.b32 m, %3, %4;\n"
+      " setp.ne.u32 q, m, 0;\n"
+      " @q st.global.cs.v2.f32 [%0], {%1, %2};\n}" ::"l"(p),
+      "f"(v.re), "f"(v.im), "r"(mask), "n"(BIT)
+      : "memory");
+}
+template <unsigned BIT>
+__device__ __forceinline__ void st_cs_mask(Cpx<double>* p, Cpx<double> v,
+                                           unsigned mask) {
+  asm volatile(
+      "{\n .reg .pred q;\n .reg .b32 m;\n and.b32 m, %3, %4;\n"
+      " setp.ne.u32 q, m, 0;\n"
+      " @q st.global.cs.v2.f64 [%0], {%1, %2};\n}" ::"l"(p),
+      "d"(v.re), "d"(v.im), "r"(mask), "n"(BIT)
+      : "memory");
+}
 __device__ __forceinline__ void st_cs_if(Cpx<double>* p, Cpx<double> v,
                                          unsigned o, unsigned span) {
   asm volatile(
@@ -630,6 +651,15 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     const unsigned span =
         (!live || (a.dbg & 1) || o_hi <= o_lo) ? 0u : unsigned(o_hi - o_lo);
     const long long w0 = g0 - a.t0 + a.origin;
+    // writeback mask (item-invariant): element e of this thread is output
+    // o = o0 + elem_part(e) of the segment, kept iff o_lo <= o < o_hi
+    const int o0 = G::thread_part(P - 1, t) - a.t0;
+    unsigned vmask = 0;
+    sfor<0, E>([&](auto ec) {
+      constexpr int e = decltype(ec)::value;
+      const unsigned o = unsigned(o0 + G::elem_part(P - 1, e) - int(o_lo));
+      vmask |= (o < span ? 1u : 0u) << e;
+    });
     const int f_lo = fc * a.fchunk;
     const int f_hi = min(a.n_fil, f_lo + a.fchunk);
     const long long nit = it + gridDim.x;
@@ -765,15 +795,12 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
       // o_lo <= o < o_hi.  With the 32-aligned engine grid every warp store
       // covers one aligned 256-byte chunk of the output row.
       {
-        constexpr int q = P - 1;
-        const int o0 = G::thread_part(q, t) - a.t0;
         const long long goff = (long long)f * a.out_ld + (g0 - a.out_base);
         Cpx<R>* orow = a.out + goff + o0;
-        const int ol = int(o_lo);
         sfor<0, E>([&](auto ec) {
           constexpr int e = decltype(ec)::value;
-          constexpr int pe = G::elem_part(q, e);
-          st_cs_if(orow + pe, y[e], unsigned(o0 + pe - ol), span);
+          constexpr int pe = G::elem_part(P - 1, e);
+          st_cs_mask<(1u << e)>(orow + pe, y[e], vmask);
         });
       }
     }

@@ -4,7 +4,7 @@
 // validates its arguments, dispatches the runtime FFT length and precision to
 // a template instantiation and launches on the caller's stream.  Kernel
 // shapes (policies) are chosen per N from measurements;
-// OLSB_VARIANT=k overrides the N=2048/4096 fp32 policy for tuning sweeps.
+// OLSB_VARIANT=k overrides the fp32 policy for tuning sweeps.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -13,34 +13,25 @@
 #include <mutex>
 
 #include "olsb.h"
-#include "olsb_engine.cuh"
+#include "olsb_launch.cuh"
+
+// the per-length launchers live in olsb_inst.cu objects
+#define OLSB_EXTERN_ALL(L) OLSB_LAUNCHERS_ALL(extern, L)
+OLSB_EXTERN_ALL(2)
+OLSB_EXTERN_ALL(3)
+OLSB_EXTERN_ALL(4)
+OLSB_EXTERN_ALL(5)
+OLSB_EXTERN_ALL(6)
+OLSB_EXTERN_ALL(7)
+OLSB_EXTERN_ALL(8)
+OLSB_EXTERN_ALL(9)
+OLSB_EXTERN_ALL(10)
+OLSB_EXTERN_ALL(11)
+OLSB_EXTERN_ALL(12)
 
 namespace olsb {
 
-// ---------------------------------------------------------------------------
-// launch helpers
-// ---------------------------------------------------------------------------
-inline int num_sms() {
-  int dev = 0, n = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  return n > 0 ? n : 1;
-}
-
-template <class K>
-int prepare(K kernel, size_t smem, int threads, int* resident) {
-  cudaError_t e = cudaFuncSetAttribute(
-      kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (e != cudaSuccess) return int(e);
-  int occ = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads,
-                                                    smem);
-  if (e != cudaSuccess) return int(e);
-  *resident = std::max(1, occ) * num_sms();
-  return 0;
-}
-
-static int g_filter_chunk = 0;
+int g_filter_chunk = 0;
 
 // Texture objects over engine-layout spectra (H_TEX), cached per
 // (device, pointer, size); creating one costs microseconds, so a FilterSet
@@ -55,7 +46,7 @@ static std::mutex g_tex_mu;
 static TexKey g_tex_cache[64];
 static int g_tex_n = 0;
 
-inline int spectra_texture(const void* ptr, size_t bytes,
+int spectra_texture(const void* ptr, size_t bytes,
                            cudaTextureObject_t* out) {
   int dev = 0;
   cudaGetDevice(&dev);
@@ -87,137 +78,6 @@ inline int spectra_texture(const void* ptr, size_t bytes,
   g_tex_cache[g_tex_n++] = TexKey{dev, ptr, bytes, tex};
   *out = tex;
   return 0;
-}
-
-// default fused-kernel policy per (precision, N)
-template <class R, int LOGN>
-struct DefaultPolicy {
-  static constexpr bool dbl = std::is_same<R, double>::value;
-  static constexpr int T = Geo<LOGN>::T;
-  // fp32 (OLSB_VARIANT=2 / 3 of the sweep in DESIGN.md §5): 128-thread CTAs,
-  // 4 CTAs per SM, segment spectrum and runtime-window twiddles in TMEM, the
-  // next filter's spectrum prefetched through the TEX path; N = 4096 double
-  // buffers the exchange (one barrier per exchange).
-  static constexpr int SEGS = dbl ? std::max(1, 256 / T) : std::max(1, 128 / T);
-  using type = KCfg<R, LOGN, SEGS, (!dbl && LOGN == 12) ? 2 : 1,
-                    dbl ? H_LDG : H_TEX, 0,
-                    dbl ? 1 : std::max(1, 512 / (SEGS * T)), 0, dbl ? 0 : 2,
-                    dbl ? 0 : 1>;
-};
-
-// tuning variants for fp32 (OLSB_VARIANT).  A CTA holds SEGS x max(1,
-// 128 / T) segments; MINB is CTAs per SM for a 128-thread CTA.
-template <int LOGN, int V>
-struct Variant {
-  static constexpr int T = Geo<LOGN>::T;
-  // {SEGS, NBUF, HM, BAR, MINB, MIDREG, TMX, PREF}
-  static constexpr int tab[8][8] = {
-      {1, 1, H_TEX, 0, 4, 0, 0, 0}, {1, 1, H_TEX, 0, 4, 0, 1, 1},
-      {1, 1, H_TEX, 0, 4, 0, 2, 1}, {1, 2, H_TEX, 0, 4, 0, 2, 1},
-      {1, 1, H_TEX, 0, 5, 0, 1, 0}, {1, 2, H_TEX, 0, 4, 0, 1, 1},
-      {2, 1, H_TEX, 1, 2, 0, 2, 1}, {1, 1, H_TEX, 0, 8, 0, 1, 0}};
-  static constexpr int segs = tab[V][0] * std::max(1, 128 / T);
-  static constexpr int minb = std::max(1, tab[V][4] * 128 / (segs * T));
-  using type = KCfg<float, LOGN, segs, tab[V][1], tab[V][2], tab[V][3], minb,
-                    tab[V][5], tab[V][6], tab[V][7]>;
-};
-
-inline int debug_env() {
-  static int v = [] {
-    const char* e = getenv("OLSB_DEBUG");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
-}
-
-inline int variant_env() {
-  static int v = [] {
-    const char* e = getenv("OLSB_VARIANT");
-    return e ? atoi(e) : -1;
-  }();
-  return v;
-}
-
-template <class C>
-int launch_fused_cfg(FusedArgs<typename C::R> a, cudaStream_t st) {
-  auto kern = fused_c2c_kernel<C>;
-  int resident = 0;
-  int rc = prepare(kern, C::f_smem_bytes, C::THREADS, &resident);
-  if (rc) return rc;
-  // the occupancy API reports one CTA per SM for kernels that allocate
-  // tensor memory; the TMEM policies size their columns for MINB CTAs/SM
-  if constexpr (C::TMX) resident = std::max(resident, C::MINB * num_sms());
-  if constexpr (C::HM == H_TEX) {
-    rc = spectra_texture(a.spec, size_t(a.n_fil) * C::VPT * C::T * 16, &a.htex);
-    if (rc) return rc;
-  }
-  a.fchunk = (g_filter_chunk > 0 && g_filter_chunk < a.n_fil) ? g_filter_chunk
-                                                              : a.n_fil;
-  const long long nseg = a.k_hi - a.k_lo;
-  const long long ngroups = (nseg + C::SEGS - 1) / C::SEGS;
-  const long long nitems = ngroups * ((a.n_fil + a.fchunk - 1) / a.fchunk);
-  const int grid = int(std::min<long long>(nitems, resident));
-  if (grid <= 0) return 0;
-  kern<<<grid, C::THREADS, C::f_smem_bytes, st>>>(a);
-  return int(cudaGetLastError());
-}
-
-template <class R, int LOGN>
-int launch_fused(FusedArgs<R> a, cudaStream_t st) {
-  if constexpr (std::is_same<R, float>::value) {
-    switch (variant_env()) {
-      case 0: return launch_fused_cfg<typename Variant<LOGN, 0>::type>(a, st);
-      case 1: return launch_fused_cfg<typename Variant<LOGN, 1>::type>(a, st);
-      case 2: return launch_fused_cfg<typename Variant<LOGN, 2>::type>(a, st);
-      case 3: return launch_fused_cfg<typename Variant<LOGN, 3>::type>(a, st);
-      case 4: return launch_fused_cfg<typename Variant<LOGN, 4>::type>(a, st);
-      case 5: return launch_fused_cfg<typename Variant<LOGN, 5>::type>(a, st);
-      case 6: return launch_fused_cfg<typename Variant<LOGN, 6>::type>(a, st);
-      case 7: return launch_fused_cfg<typename Variant<LOGN, 7>::type>(a, st);
-      default: break;
-    }
-  }
-  return launch_fused_cfg<typename DefaultPolicy<R, LOGN>::type>(a, st);
-}
-
-template <class R, int LOGN>
-int launch_fwd_rows(RowsArgs<R> a, cudaStream_t st) {
-  using C = RowCfg<R, LOGN>;
-  auto kern = fwd_rows_kernel<C>;
-  int resident = 0;
-  int rc = prepare(kern, C::smem_bytes, C::THREADS, &resident);
-  if (rc) return rc;
-  const int ngroups = (a.rows + C::SEGS - 1) / C::SEGS;
-  const int grid = std::min(ngroups, resident);
-  if (grid <= 0) return 0;
-  kern<<<grid, C::THREADS, C::smem_bytes, st>>>(a);
-  return int(cudaGetLastError());
-}
-
-template <class R, int LOGN>
-int launch_inv_rows(const Cpx<R>* in, Cpx<R>* out, int rows, cudaStream_t st) {
-  using C = RowCfg<R, LOGN>;
-  auto kern = inv_rows_kernel<C>;
-  int resident = 0;
-  int rc = prepare(kern, C::smem_bytes, C::THREADS, &resident);
-  if (rc) return rc;
-  const int ngroups = (rows + C::SEGS - 1) / C::SEGS;
-  const int grid = std::min(ngroups, resident);
-  if (grid <= 0) return 0;
-  kern<<<grid, C::THREADS, C::smem_bytes, st>>>(in, out, rows);
-  return int(cudaGetLastError());
-}
-
-template <class R, int LOGN>
-int launch_perm_to_dev(const Cpx<R>* perm, void* dev, int rows,
-                       cudaStream_t st) {
-  using C = RowCfg<R, LOGN>;
-  const long long total = (long long)rows * C::VPT * C::T;
-  if (total == 0) return 0;
-  const int grid = int(std::min<long long>((total + 255) / 256, 4096));
-  perm_to_dev_kernel<C><<<grid, 256, 0, st>>>(
-      perm, reinterpret_cast<typename V16<R>::type*>(dev), rows);
-  return int(cudaGetLastError());
 }
 
 inline int log2_of(int n) {
