@@ -145,19 +145,24 @@ __device__ __forceinline__ void group_sync(int sl) {
 // ---------------------------------------------------------------------------
 // shared-memory window I/O (addresses = per-thread base + immediates)
 // ---------------------------------------------------------------------------
-template <class C, int Q>
+template <class C, int Q, int X>
 __device__ __forceinline__ void smem_store(Cpx<typename C::R>* __restrict__ seg_buf,
                                            int t, const Cpx<typename C::R>* x) {
   using R = typename C::R;
   using G = typename C::G;
-  using L = typename C::L;
+  using L = XLayout<R, C::LOGN, X>;
+  constexpr int pb = L::pair_bit(Q);
   Cpx<R>* b = seg_buf + L::pos(G::thread_part(Q, t));
-  if constexpr (Q == 0 && !C::dbl && C::E >= 2) {
-    sfor<0, C::E / 2>([&](auto ec) {
-      constexpr int e = 2 * decltype(ec)::value;
-      constexpr int off = L::pos(G::elem_part(Q, e));
-      *reinterpret_cast<float4*>(b + off) =
-          make_float4(x[e].re, x[e].im, x[e + 1].re, x[e + 1].im);
+  if constexpr (pb >= 0 && !C::dbl && C::E >= 2) {
+    // 128-bit: samples e and e | 2^pb are adjacent in shared memory
+    sfor<0, C::E>([&](auto ec) {
+      constexpr int e = decltype(ec)::value;
+      if constexpr (!((e >> pb) & 1)) {
+        constexpr int off = L::pos(G::elem_part(Q, e));
+        constexpr int e1 = e | (1 << pb);
+        *reinterpret_cast<float4*>(b + off) =
+            make_float4(x[e].re, x[e].im, x[e1].re, x[e1].im);
+      }
     });
   } else {
     sfor<0, C::E>([&](auto ec) {
@@ -168,20 +173,24 @@ __device__ __forceinline__ void smem_store(Cpx<typename C::R>* __restrict__ seg_
   }
 }
 
-template <class C, int Q>
+template <class C, int Q, int X>
 __device__ __forceinline__ void smem_load(const Cpx<typename C::R>* __restrict__ seg_buf,
                                           int t, Cpx<typename C::R>* x) {
   using R = typename C::R;
   using G = typename C::G;
-  using L = typename C::L;
+  using L = XLayout<R, C::LOGN, X>;
+  constexpr int pb = L::pair_bit(Q);
   const Cpx<R>* b = seg_buf + L::pos(G::thread_part(Q, t));
-  if constexpr (Q == 0 && !C::dbl && C::E >= 2) {
-    sfor<0, C::E / 2>([&](auto ec) {
-      constexpr int e = 2 * decltype(ec)::value;
-      constexpr int off = L::pos(G::elem_part(Q, e));
-      const float4 v = *reinterpret_cast<const float4*>(b + off);
-      x[e] = Cpx<R>{v.x, v.y};
-      x[e + 1] = Cpx<R>{v.z, v.w};
+  if constexpr (pb >= 0 && !C::dbl && C::E >= 2) {
+    sfor<0, C::E>([&](auto ec) {
+      constexpr int e = decltype(ec)::value;
+      if constexpr (!((e >> pb) & 1)) {
+        constexpr int off = L::pos(G::elem_part(Q, e));
+        constexpr int e1 = e | (1 << pb);
+        const float4 v = *reinterpret_cast<const float4*>(b + off);
+        x[e] = Cpx<R>{v.x, v.y};
+        x[e1] = Cpx<R>{v.z, v.w};
+      }
     });
   } else {
     sfor<0, C::E>([&](auto ec) {
@@ -442,12 +451,13 @@ __device__ __forceinline__ void exchange(Cpx<typename C::R>* bufs, int& xc,
                                          const H2& post_bar = H2{}) {
   Cpx<typename C::R>* buf = bufs + (C::NBUF == 2 ? (xc & 1) * C::buf_elems : 0) +
                             size_t(sl) * C::L::stride;
+  constexpr int X = QW < QR ? QW : QR;  // exchange between windows X, X+1
   if constexpr (C::NBUF == 1) group_sync<C>(sl);
-  smem_store<C, QW>(buf, t, x);
+  smem_store<C, QW, X>(buf, t, x);
   pre_bar();
   group_sync<C>(sl);
   post_bar();
-  smem_load<C, QR>(buf, t, x);
+  smem_load<C, QR, X>(buf, t, x);
   ++xc;
 }
 

@@ -149,14 +149,57 @@ constexpr Pad pad_for(bool dbl, int logn) {
   return dbl ? d[logn] : f[logn];
 }
 
+// Per-exchange layouts (exchange X moves a segment between windows X and
+// X+1).  fp32, N = 512..2048: index bit `rb` becomes address bit 0, so a
+// 128-bit access pairs two samples that differ in that bit; plo / phi are the
+// element bits paired on the lower / upper window side (-1: 64-bit access).
+// Exchange 0 pairs on an index bit both windows hold in registers (the
+// junction's batch bits), so both sides are 128-bit; exchange 1 pairs on the
+// upper window's element bit 0.  Found by tools/smem_layout_search.py
+// (xsearch), zero bank conflicts; other cases use pad_for with the junction
+// side paired on bit 0.
+struct XPad {
+  int rb, k1, p1, k2, p2, k3, p3, plo, phi, span;
+};
+constexpr XPad xpad_for(bool dbl, int logn, int x) {
+  if (!dbl && logn == 9)
+    return x == 0 ? XPad{1, 4, 2, 4, 0, 4, 0, 1, 0, 574}
+                  : XPad{5, 6, 4, 6, 0, 6, 0, -1, 0, 540};
+  if (!dbl && logn == 10)
+    return x == 0 ? XPad{2, 4, 2, 4, 0, 4, 0, 2, 0, 1150}
+                  : XPad{6, 7, 8, 7, 0, 7, 0, -1, 0, 1080};
+  if (!dbl && logn == 11)
+    return x == 0 ? XPad{3, 4, 2, 9, 4, 9, 0, 3, 0, 2314}
+                  : XPad{7, 9, 4, 9, 0, 9, 0, -1, 0, 2060};
+  const Pad pd = pad_for(dbl, logn);
+  return XPad{0,     pd.k1, pd.p1, pd.k2, pd.p2, pd.k3, pd.p3,
+              (!dbl && x == 0) ? 0 : -1, -1, pd.stride};
+}
+
+template <class R, int LOGN, int X>
+struct XLayout {
+  static constexpr XPad xp = xpad_for(std::is_same<R, double>::value, LOGN, X);
+  static OLSB_HD constexpr int rot(int p) {
+    return xp.rb == 0 ? p
+                      : ((p >> (xp.rb + 1)) << (xp.rb + 1)) |
+                            ((p & ((1 << xp.rb) - 1)) << 1) | ((p >> xp.rb) & 1);
+  }
+  static OLSB_HD constexpr int pos(int p) {
+    return rot(p) + xp.p1 * (rot(p) >> xp.k1) + xp.p2 * (rot(p) >> xp.k2) +
+           xp.p3 * (rot(p) >> xp.k3);
+  }
+  // paired element bit for an access from window q (X or X+1)
+  static constexpr int pair_bit(int q) { return q == X ? xp.plo : xp.phi; }
+};
+
 template <class R, int LOGN>
 struct SmemLayout {
-  static constexpr Pad pd = pad_for(std::is_same<R, double>::value, LOGN);
-  static OLSB_HD constexpr int pos(int p) {
-    return p + pd.p1 * (p >> pd.k1) + pd.p2 * (p >> pd.k2) +
-           pd.p3 * (p >> pd.k3);
-  }
-  static constexpr int stride = pd.stride;  // per segment, in Cpx<R> units
+  // buffer stride per segment (Cpx<R> units): the largest exchange layout
+  static constexpr int stride =
+      xpad_for(std::is_same<R, double>::value, LOGN, 0).span >
+              xpad_for(std::is_same<R, double>::value, LOGN, 1).span
+          ? xpad_for(std::is_same<R, double>::value, LOGN, 0).span
+          : xpad_for(std::is_same<R, double>::value, LOGN, 1).span;
 };
 
 // ---------------------------------------------------------------------------

@@ -61,16 +61,17 @@ struct DefaultPolicy {
 };
 
 // tuning variants for fp32 (OLSB_VARIANT).  A CTA holds SEGS x max(1,
-// 128 / T) segments; MINB is CTAs per SM for a 128-thread CTA.
+// 128 / T) segments; MINB is the target number of 128-thread warpgroups per
+// SM (CTAs per SM = MINB x 128 / CTA threads).
 template <int LOGN, int V>
 struct Variant {
   static constexpr int T = Geo<LOGN>::T;
-  // {SEGS, NBUF, HM, BAR, MINB, MIDREG, TMX, PREF}
+  // {SEGS, NBUF, HM, BAR, MINB (warpgroups/SM), MIDREG, TMX, PREF}
   static constexpr int tab[8][8] = {
       {1, 1, H_TEX, 0, 4, 0, 0, 0}, {1, 1, H_TEX, 0, 4, 0, 1, 1},
       {1, 1, H_TEX, 0, 4, 0, 2, 1}, {1, 2, H_TEX, 0, 4, 0, 2, 1},
       {1, 1, H_TEX, 0, 5, 0, 1, 0}, {1, 2, H_TEX, 0, 4, 0, 1, 1},
-      {2, 1, H_TEX, 1, 2, 0, 2, 1}, {1, 1, H_TEX, 0, 8, 0, 1, 0}};
+      {2, 1, H_TEX, 1, 4, 0, 2, 1}, {2, 1, H_TEX, 0, 4, 0, 2, 1}};
   static constexpr int segs = tab[V][0] * std::max(1, 128 / T);
   static constexpr int minb = std::max(1, tab[V][4] * 128 / (segs * T));
   using type = KCfg<float, LOGN, segs, tab[V][1], tab[V][2], tab[V][3], minb,

@@ -98,4 +98,10 @@ void emu_pad(int dbl, int logn, int* out7) {
   out7[5] = pd.p3;
   out7[6] = pd.stride;
 }
+// per-exchange layout probe: rb, k1, p1, k2, p2, k3, p3, plo, phi, span
+void emu_xpad(int dbl, int logn, int x, int* out10) {
+  const XPad p = xpad_for(dbl != 0, logn, x);
+  const int v[10] = {p.rb, p.k1, p.p1, p.k2, p.p2, p.k3, p.p3, p.plo, p.phi, p.span};
+  for (int i = 0; i < 10; ++i) out10[i] = v[i];
+}
 }

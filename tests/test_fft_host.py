@@ -88,3 +88,28 @@ def test_smem_layout_conflict_free_and_injective(emu, dbl, logn):
     loge, logt, _, _, _ = S.geo(logn)
     segs = max(1, 256 >> logt)
     assert S.conflict_free(logn, min(segs, 64), *kp, stride, bool(dbl))
+
+
+@pytest.mark.parametrize("dbl", [0, 1])
+@pytest.mark.parametrize("logn", range(5, 13))
+def test_exchange_layouts_conflict_free(emu, dbl, logn):
+    """Every per-exchange layout (xpad_for) is injective, fits the buffer
+    stride, keeps 128-bit pairs adjacent and 16-byte aligned, and is
+    bank-conflict free for both window sides of the exchange."""
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import smem_layout_search as S
+    loge, logt, npass, g0, los = S.geo(logn)
+    if logt < 5:
+        pytest.skip("several segments per warp: covered by the pad_for test")
+    n = 1 << logn
+    for x in range(npass - 1):
+        v = (ctypes.c_int * 10)()
+        emu.emu_xpad(dbl, logn, x, v)
+        rb, k1, p1, k2, p2, k3, p3, plo, phi, span = list(v)
+        kp = [k1, p1, k2, p2, k3, p3]
+        pos = [S.xpos(p, rb, kp) for p in range(n)]
+        assert len(set(pos)) == n and max(pos) < span
+        if dbl:
+            continue   # fp64 keeps pad_for (checked above)
+        sides = [(x, None if plo < 0 else plo), (x + 1, None if phi < 0 else phi)]
+        assert S.xconflict_free(logn, rb, kp, sides)

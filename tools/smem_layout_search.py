@@ -118,7 +118,86 @@ def search(logn, segs, dbl, nterms=2):
     return best
 
 
+# ---------------------------------------------------------------------------
+# Per-exchange layouts (olsb_fft.cuh xpad_for): index bit b is rotated to
+# address bit 0 so 128-bit accesses pair samples differing in that bit.
+# `sides` = [(window, paired element bit or None for 64-bit), ...].
+# ---------------------------------------------------------------------------
+def rot(p, b):
+    # move index bit b to address bit 0
+    if b == 0: return p
+    return ((p >> (b + 1)) << (b + 1)) | ((p & ((1 << b) - 1)) << 1) | ((p >> b) & 1)
+
+def xpos(p, b, kp):
+    q = rot(p, b)
+    return q + sum(kp[i+1] * (q >> kp[i]) for i in range(0, len(kp), 2))
+
+def accesses(logn, q, pb):
+    """(width_elems, lanes_per_phase, units) and element groups for window q;
+    pb = element bit paired in 128-bit accesses (None = 64-bit)"""
+    loge, logt, npass, g0, los = geo(logn)
+    E = 1 << loge
+    if pb is None:
+        return 1, 16, 16, [(e,) for e in range(E)]
+    return 2, 8, 8, [(e, e | (1 << pb)) for e in range(E) if not (e >> pb) & 1]
+
+def xconflict_free(logn, b, kp, sides):
+    loge, logt, npass, g0, los = geo(logn)
+    T = 1 << logt
+    for (q, pb) in sides:
+        w, lpp, bu, groups = accesses(logn, q, pb)
+        for g in groups:
+            for w0 in range(0, T, 32):
+                for ph in range(0, 32, lpp):
+                    seen = {}
+                    for lane in range(ph, ph + lpp):
+                        t = w0 + lane
+                        if t >= T: continue
+                        a = xpos(index(logn, q, g[0], t), b, kp)
+                        if w == 2:
+                            a2 = xpos(index(logn, q, g[1], t), b, kp)
+                            if a % 2 or a2 != a + 1: return False
+                            unit, key = (a // 2) % bu, a // 2
+                        else:
+                            unit, key = a % bu, a
+                        if unit in seen and seen[unit] != key: return False
+                        seen[unit] = key
+    return True
+
+def xsearch(logn, b, sides, nterms):
+    best = None
+    ks = range(1, logn + 1)
+    pads = [0, 2, 4, 6, 8, 12, 16]
+    for K in itertools.combinations(ks, nterms):
+        for P in itertools.product(pads, repeat=nterms):
+            kp = [v for pair in zip(K, P) for v in pair]
+            span = xpos((1 << logn) - 1, b, kp) + 1
+            if best and span >= best[0]: continue
+            if xconflict_free(logn, b, kp, sides):
+                best = (span + (span & 1), kp)
+    return best
+
+def xmain():
+    for logn in (9, 10, 11, 12):
+        loge, logt, npass, g0, los = geo(logn)
+        if g0 < 4:   # junction batch bits overlap window 1
+            bA, sidesA = los[1], [(0, los[1]), (1, 0)]
+        else:
+            bA, sidesA = 0, [(0, 0), (1, None)]
+        bB, sidesB = los[2], [(1, None), (2, 0)]
+        for name, b, sides in (("A", bA, sidesA), ("B", bB, sidesB)):
+            res = None
+            for nt in (1, 2, 3):
+                res = xsearch(logn, b, sides, nt)
+                if res:
+                    break
+            print(logn, name, "rotbit", b, sides, res, flush=True)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "x":
+        xmain()
+        sys.exit(0)
     out = []
     for dbl in (False, True):
         for logn in range(2, 13):
