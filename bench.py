@@ -71,7 +71,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -170,12 +170,13 @@ def run_reference(args, rank: int):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cufft", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -330,6 +331,31 @@ def main():
                        " streaming chunks" if world == 1 else
                        "per-rank H2D shard + fused_range + D2H"}
 
+    # ---- the paper's comparison point: cuFFT-based OLS (Algorithm 1,
+    # convolve(variant="pipelined")) on the same shard, same N
+    cufft = None
+    if not args.no_cufft:
+        pc = ob.plan(n_own, M, "c2c", 0, NFFT)
+        sig_own = ob.make_signal(own, "complex", P)
+        fc = ob.transform_filters(ob.make_filterset(taps, 0, P, device=dev),
+                                  pc, "natural")
+        ob.convolve(sig_own, fc, pc, variant="pipelined", out=out)
+        torch.cuda.synchronize()
+        c_ms = []
+        for _ in range(3):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            ob.convolve(sig_own, fc, pc, variant="pipelined", out=out)
+            e1.record()
+            e1.synchronize()
+            c_ms.append(e0.elapsed_time(e1))
+        cm = statistics.median(c_ms)
+        cufft = {"ms_per_step": cm, "value": n_own * NFIL / (cm * 1e-3) * world,
+                 "unit": "samples/s", "speedup_fused": cm / kmean,
+                 "path": "gather -> batched C2C cuFFT -> multiply -> batched "
+                         "inverse C2C -> discard (chunked), same N"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
@@ -360,6 +386,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": args.steps,
+            "cufft_ols": cufft,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
