@@ -1,0 +1,66 @@
+// Does a store stream overlap with FP32 work on B200?  Each warp repeats:
+// FP work (K packed FFMA2 on 8 independent chains) then 16 coalesced 256-B
+// stores (st.global.cs.v2), like the fused kernel's filter loop.  Reports
+// time for FP only, stores only, and both, with 4 x 128-thread CTAs per SM
+// and the cfg3 output volume (6 GiB).
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+typedef unsigned long long u64;
+__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
+  u64 d;
+  asm volatile("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+template <int MODE, int K>
+__global__ void __launch_bounds__(128, 4) k(float2* out, long long rows, int row_len) {
+  // a "row" = one (segment, filter): 128 threads x 16 samples
+  u64 acc[8];
+  for (int i = 0; i < 8; ++i) acc[i] = threadIdx.x + i;
+  const u64 s = 0x3f8000003f800000ull;
+  for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
+    if (MODE & 1) {
+#pragma unroll 1
+      for (int it = 0; it < K / 8; ++it)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = fma2(acc[i], s, acc[(i + 1) & 7]);
+    }
+    if (MODE & 2) {
+      float2* p = out + r * (long long)row_len + threadIdx.x;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        float2 v = make_float2(__uint_as_float((unsigned)acc[e & 7]), 1.f);
+        asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" ::"l"(p + e * 128), "f"(v.x), "f"(v.y) : "memory");
+      }
+    }
+  }
+  if (acc[0] == 12345) out[0] = make_float2(1, 1);
+}
+int main() {
+  int sms;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const long long rows = 5141LL * 96;  // cfg3 segment-filters
+  const int row_len = 2048;
+  float2* out;
+  cudaMalloc(&out, rows * row_len * sizeof(float2));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  auto run = [&](const char* nm, auto kern) {
+    float ms = 0;
+    for (int rep = 0; rep < 3; ++rep) {
+      cudaEventRecord(e0);
+      kern<<<sms * 4, 128>>>(out, rows, row_len);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      cudaEventElapsedTime(&ms, e0, e1);
+    }
+    printf("%-28s %.3f ms  %s\n", nm, ms, cudaGetErrorString(cudaGetLastError()));
+  };
+  run("fp only   K=280", k<1, 280>);
+  run("store only", k<2, 280>);
+  run("fp+store  K=280", k<3, 280>);
+  run("fp only   K=200", k<1, 200>);
+  run("fp+store  K=200", k<3, 200>);
+  return 0;
+}

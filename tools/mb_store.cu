@@ -1,65 +1,90 @@
-// Store-pattern microbenchmark for the OLS output writes (no FFT).
-// Each CTA (128 threads) writes, per (segment, filter), L valid samples of
-// out[f][s*L + o].  Modes vary what the fused kernel could do differently.
+// Write-bandwidth microbenchmark for the OLS output stream: every warp writes
+// aligned 256-byte chunks (32 lanes x 8 B), like the fused kernel's
+// writeback.  Variants: store width / cache policy / TMA bulk store.
 #include <cstdio>
+#include <cstdint>
 #include <cuda_runtime.h>
-// mode 0: fused pattern: p = t + 128 e (16 x 8 B per thread), o = p - t0
-// mode 2: 16-byte stores: thread writes o = 2 t + 256 e, o + 1 (8 x 16 B)
+
 template <int MODE>
-__global__ void __launch_bounds__(128, 4) k(float2* out, long long ns, int L,
-                                            int t0, int nseg, int F, long long ld) {
-  int t = threadIdx.x;
-  for (int s = blockIdx.x; s < nseg; s += gridDim.x) {
-    long long g0 = (long long)s * L;
-    unsigned span = (unsigned)min((long long)L, ns - g0);
-    for (int f = 0; f < F; ++f) {
-      if (MODE == 0) {
-        float2* row = out + (long long)f * ld + g0 + t - t0;
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          unsigned o = t + 128 * e - t0;
-          if (o < span) __stcs(row + 128 * e, make_float2(s + e, f + t));
-        }
-      } else {
-        float2* row = out + (long long)f * ld + g0;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          unsigned o = 2 * t + 256 * e;
-          if (o + 1 < span) __stcs(reinterpret_cast<float4*>(row + o), make_float4(s, e, f, t));
-          else if (o < span) __stcs(row + o, make_float2(s, e));
-        }
-      }
+__global__ void __launch_bounds__(128) wr(float2* out, long long n2, int iters) {
+  // grid-stride over 256-B chunks; 16 chunks per warp per iteration like the
+  // kernel's 16 stores per filter
+  const long long nch = n2 / 32;
+  const int lane = threadIdx.x & 31;
+  const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 32;
+  const long long nw = (gridDim.x * (long long)blockDim.x) / 32;
+  float2 v = make_float2(lane * 1.f, 2.f);
+  for (long long c = w; c < nch; c += nw) {
+    float2* p = out + c * 32 + lane;
+    if (MODE == 0) {
+      asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
+    } else if (MODE == 1) {
+      asm volatile("st.global.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
+    } else if (MODE == 2) {
+      asm volatile("st.global.L1::no_allocate.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
     }
   }
 }
-int main() {
-  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
-  long long total = (1LL << 23) * 96;
-  float2* out; cudaMalloc(&out, total * 8 + 4096);
-  struct Case { const char* name; long long ns; int F; int L; int mode; int grid; };
-  Case cases[] = {
-    {"fused F=96 L=1649 p592", 1 << 23, 96, 1649, 0, 592},
-    {"fused F=96 L=1649 g5088", 1 << 23, 96, 1649, 0, 5088},
-    {"one row L=1649 g5088", total, 1, 1649, 0, 1 << 20},
-    {"F=96 L=2048 aligned g4096", 1 << 23, 96, 2048, 0, 4096},
-    {"F=96 L=1649 16B g5088", 1 << 23, 96, 1649, 2, 5088},
-    {"F=96 L=1648 16B g5091", 1 << 23, 96, 1648, 2, 5091},
-    {"F=96 L=2048 16B g4096", 1 << 23, 96, 2048, 2, 4096},
-  };
-  for (auto& c : cases) {
-    int nseg = int((c.ns + c.L - 1) / c.L);
-    int t0 = 2048 - c.L;
-    for (int w = 0; w < 2; ++w) {
-      cudaEventRecord(a);
-      if (c.mode == 0) k<0><<<c.grid, 128>>>(out, c.ns, c.L, t0, nseg, c.F, c.ns);
-      else k<2><<<c.grid, 128>>>(out, c.ns, c.L, t0, nseg, c.F, c.ns);
-      cudaEventRecord(b); cudaEventSynchronize(b);
-      float ms; cudaEventElapsedTime(&ms, a, b);
-      if (w) printf("%-28s %.3f ms  %.0f GB/s\n", c.name, ms, c.ns * c.F * 8 / ms / 1e6);
-    }
+// v4: each lane writes 16 B (two warps' worth of chunks per instruction)
+__global__ void __launch_bounds__(128) wr4(float4* out, long long n4) {
+  const long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long st = gridDim.x * (long long)blockDim.x;
+  for (long long i = i0; i < n4; i += st) {
+    asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(out + i), "f"(1.f), "f"(2.f), "f"(3.f), "f"(4.f) : "memory");
   }
-  cudaEventRecord(a); cudaMemsetAsync(out, 0, total * 8); cudaEventRecord(b); cudaEventSynchronize(b);
-  float ms; cudaEventElapsedTime(&ms, a, b); printf("memset                       %.3f ms  %.0f GB/s\n", ms, total * 8 / ms / 1e6);
-  printf("%s\n", cudaGetErrorString(cudaGetLastError()));
+}
+// TMA bulk store: each CTA writes 8 KB tiles from shared memory
+__global__ void __launch_bounds__(128) wr_tma(char* out, long long bytes) {
+  __shared__ __align__(128) float4 tile[512];  // 8 KB
+  for (int i = threadIdx.x; i < 512; i += 128) tile[i] = make_float4(1, 2, 3, 4);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const long long ntile = bytes / 8192;
+    for (long long tt = blockIdx.x; tt < ntile; tt += gridDim.x) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 8192;" ::"l"(out + tt * 8192),
+                   "r"((uint32_t)__cvta_generic_to_shared(tile)) : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 8;" ::: "memory");
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+}
+
+int main() {
+  int sms;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const long long bytes = 6442450944LL;  // cfg3 output: 96 x 2^23 x 8 B
+  char* buf;
+  if (cudaMalloc(&buf, bytes) != cudaSuccess) { printf("alloc failed\n"); return 1; }
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  auto run = [&](const char* name, auto launch) {
+    for (int rep = 0; rep < 3; ++rep) {
+      cudaEventRecord(e0);
+      launch();
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (rep == 2) printf("%-34s %.3f ms  %.0f GB/s  %s\n", name, ms, bytes / ms / 1e6,
+                           cudaGetErrorString(cudaGetLastError()));
+    }
+  };
+  const long long n2 = bytes / 8;
+  for (int per : {4, 8, 16}) {
+    char nm[64];
+    snprintf(nm, 64, "st.cs.v2   %2d CTA/SM", per);
+    run(nm, [&] { wr<0><<<sms * per, 128>>>((float2*)buf, n2, 1); });
+    snprintf(nm, 64, "st.v2      %2d CTA/SM", per);
+    run(nm, [&] { wr<1><<<sms * per, 128>>>((float2*)buf, n2, 1); });
+    snprintf(nm, 64, "st.noalloc %2d CTA/SM", per);
+    run(nm, [&] { wr<2><<<sms * per, 128>>>((float2*)buf, n2, 1); });
+    snprintf(nm, 64, "st.cs.v4   %2d CTA/SM", per);
+    run(nm, [&] { wr4<<<sms * per, 128>>>((float4*)buf, bytes / 16); });
+  }
+  run("tma bulk 8KB x 16 CTA/SM", [&] { wr_tma<<<sms * 16, 128>>>(buf, bytes); });
+  run("cudaMemsetAsync", [&] { cudaMemsetAsync(buf, 0, bytes); });
   return 0;
 }
