@@ -36,6 +36,7 @@ extern "C" {
 
 #define OLSB_PP_NONE 0  /* postproc.py:15  KINDS[0] "none"  */
 #define OLSB_PP_SCALE 1 /* postproc.py:15  KINDS[1] "scale" */
+#define OLSB_PP_MAG2 2  /* postproc.py:15  KINDS[2] "magnitude_squared" */
 
 /* Library version (major * 10000 + minor * 100 + patch). */
 int olsb_version(void);
@@ -112,10 +113,54 @@ int olsb_fused_c2c_range(const void* x, int64_t x_base, int64_t n_s,
                          double pp_c, void* out, int64_t out_ld,
                          int64_t out_base, int precision, void* stream);
 
+/* The fused engine's |y|^2 epilogue (postproc "magnitude_squared" on the
+ * complex path): same arguments as olsb_fused_c2c, `out` is REAL
+ * (float/double, n_fil x out_ld).  Replaces K.fused_c2c_abs2(x, spectra, tw,
+ * twc, m, origin, l_eff, t0, win_off, seg_lo, seg_hi, h0, out, buf,
+ * spec_buf) (_kernels_nb.py:288-309). */
+int olsb_fused_c2c_abs2(const void* x, int64_t x_base, int64_t n_s,
+                        const void* spectra_dev, int n_fil, int n, int m,
+                        int origin, int64_t l_eff, int t0, int64_t win_off,
+                        int64_t seg_lo, int64_t seg_hi, void* out,
+                        int64_t out_ld, int64_t out_base, int precision,
+                        void* stream);
+
+/* The fused real path: real signal `x`, real taps (their complex spectra in
+ * the engine layout, from olsb_filter_spectra_c2c of the taps with zero
+ * imaginary parts), REAL output rows.  Two consecutive segments of the
+ * engine grid are transformed together as one complex segment (re: segment
+ * 2k, im: segment 2k+1): with real taps the complex convolution separates
+ * exactly into the two real ones, so no packed-real split/merge is needed.
+ * pp_kind: none, scale or magnitude_squared (v*v, fused_r2r pp_kind 2).
+ * Arguments as olsb_fused_c2c.  Replaces K.fused_r2r(x, spectra, tw_half,
+ * tw_half_conj, pack_tw, pack_tw_conj, m, origin, l_eff, t0, win_off,
+ * seg_lo, seg_hi, pp_kind, pp_c, h0, out, rbuf, z_scr, bins, prod)
+ * (_kernels_nb.py:312-337). */
+int olsb_fused_r2r(const void* x, int64_t x_base, int64_t n_s,
+                   const void* spectra_dev, int n_fil, int n, int m,
+                   int origin, int64_t l_eff, int t0, int64_t win_off,
+                   int64_t seg_lo, int64_t seg_hi, int pp_kind, double pp_c,
+                   void* out, int64_t out_ld, int64_t out_base,
+                   int precision, void* stream);
+
+/* Output-range form of olsb_fused_r2r (sharded / streamed real signals);
+ * reads the input extent of olsb_input_extent_r2r. */
+int olsb_fused_r2r_range(const void* x, int64_t x_base, int64_t n_s,
+                         const void* spectra_dev, int n_fil, int n, int m,
+                         int origin, int64_t g_lo, int64_t g_hi, int pp_kind,
+                         double pp_c, void* out, int64_t out_ld,
+                         int64_t out_base, int precision, void* stream);
+
 /* Input samples [*x_lo, *x_hi) that olsb_fused_c2c_range(g_lo, g_hi) reads
  * (before clipping to [0, n_s)): the shard plus its halos. */
 int olsb_input_extent(int n, int m, int origin, int64_t g_lo, int64_t g_hi,
                       int64_t* x_lo, int64_t* x_hi);
+
+/* Input samples [*x_lo, *x_hi) that olsb_fused_r2r_range(g_lo, g_hi) reads:
+ * the windows of whole segment pairs (both halves of a pair are always
+ * transformed together, which keeps results independent of the split). */
+int olsb_input_extent_r2r(int n, int m, int origin, int64_t g_lo,
+                          int64_t g_hi, int64_t* x_lo, int64_t* x_hi);
 
 /* Tuning knob (not in the reference): number of filters processed per work
  * item (0 = all).  Smaller chunks cut the tail of the last wave at the cost

@@ -36,8 +36,20 @@ SIGNATURES = {
     "olsb_fused_c2c_range": (c_int, [c_vp, c_i64, c_i64, c_vp, c_int, c_int,
                                      c_int, c_int, c_i64, c_i64, c_int, c_dbl,
                                      c_vp, c_i64, c_i64, c_int, c_vp]),
+    "olsb_fused_c2c_abs2": (c_int, [c_vp, c_i64, c_i64, c_vp, c_int, c_int,
+                                    c_int, c_int, c_i64, c_int, c_i64, c_i64,
+                                    c_i64, c_vp, c_i64, c_i64, c_int, c_vp]),
+    "olsb_fused_r2r": (c_int, [c_vp, c_i64, c_i64, c_vp, c_int, c_int, c_int,
+                               c_int, c_i64, c_int, c_i64, c_i64, c_i64, c_int,
+                               c_dbl, c_vp, c_i64, c_i64, c_int, c_vp]),
+    "olsb_fused_r2r_range": (c_int, [c_vp, c_i64, c_i64, c_vp, c_int, c_int,
+                                     c_int, c_int, c_i64, c_i64, c_int, c_dbl,
+                                     c_vp, c_i64, c_i64, c_int, c_vp]),
     "olsb_input_extent": (c_int, [c_int, c_int, c_int, c_i64, c_i64,
                                   ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
+    "olsb_input_extent_r2r": (c_int, [c_int, c_int, c_int, c_i64, c_i64,
+                                      ctypes.POINTER(c_i64),
+                                      ctypes.POINTER(c_i64)]),
     "olsb_set_filter_chunk": (c_int, [c_int]),
     "olsb_copy2d_async": (c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_i64,
                                   c_int, c_vp]),

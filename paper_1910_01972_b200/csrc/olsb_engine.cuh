@@ -525,9 +525,41 @@ struct FusedArgs {
   Cpx<R>* out;
   long long out_ld, out_base;
   int dbg;  // tuning: bit 0 = predicate off the output stores
+  // real-valued modes (FMODE_R2R: real signal and output; FMODE_ABS2:
+  // real |y|^2 output)
+  const R* xr;
+  R* outr;
 };
 
-template <class C>
+// fused-kernel data modes
+enum FMode : int {
+  FMODE_C2C = 0,   // complex signal -> complex outputs (_kernels_nb.py:265)
+  FMODE_R2R = 1,   // real signal, real taps -> real outputs; two segments per
+                   // complex transform (re: segment 2k, im: segment 2k + 1)
+  FMODE_ABS2 = 2,  // complex signal -> |y|^2 (fused_c2c_abs2, :288-309)
+};
+
+// streaming store of one real sample iff (mask & BIT)
+template <unsigned BIT>
+__device__ __forceinline__ void st_cs_mask_r(float* p, float v, unsigned mask) {
+  asm volatile(
+      "{\n .reg .pred q;\n .reg .b32 m;\n and.b32 m, %2, %3;\n"
+      " setp.ne.u32 q, m, 0;\n"
+      " @q st.global.cs.f32 [%0], %1;\n}" ::"l"(p),
+      "f"(v), "r"(mask), "n"(BIT)
+      : "memory");
+}
+template <unsigned BIT>
+__device__ __forceinline__ void st_cs_mask_r(double* p, double v, unsigned mask) {
+  asm volatile(
+      "{\n .reg .pred q;\n .reg .b32 m;\n and.b32 m, %2, %3;\n"
+      " setp.ne.u32 q, m, 0;\n"
+      " @q st.global.cs.f64 [%0], %1;\n}" ::"l"(p),
+      "d"(v), "r"(mask), "n"(BIT)
+      : "memory");
+}
+
+template <class C, int MODE = FMODE_C2C>
 __global__ void __launch_bounds__(C::THREADS, C::MINB)
     fused_c2c_kernel(const FusedArgs<typename C::R> a) {
   using R = typename C::R;
@@ -652,24 +684,32 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   for (long long it = blockIdx.x; it < nitems; it += gridDim.x) {
     const long long grp = it / nfch;
     const int fc = int(it - grp * nfch);
+    // s = segment (R2R: segment pair {2s, 2s + 1}) of this thread's group
     const long long s = a.k_lo + grp * C::SEGS + sl;
     const bool live = s < a.k_hi;
-    const long long g0 = s * a.seg_len;
-    // owned outputs o in [o_lo, o_hi) (clipped to this call's range)
-    const long long o_lo = a.g_lo > g0 ? a.g_lo - g0 : 0;
-    const long long o_hi = a.g_hi - g0 < a.seg_len ? a.g_hi - g0 : a.seg_len;
-    const unsigned span =
-        (!live || (a.dbg & 1) || o_hi <= o_lo) ? 0u : unsigned(o_hi - o_lo);
-    const long long w0 = g0 - a.t0 + a.origin;
-    // writeback mask (item-invariant): element e of this thread is output
-    // o = o0 + elem_part(e) of the segment, kept iff o_lo <= o < o_hi
+    const long long g0 = (MODE == FMODE_R2R ? 2 * s : s) * a.seg_len;
     const int o0 = G::thread_part(P - 1, t) - a.t0;
-    unsigned vmask = 0;
-    sfor<0, E>([&](auto ec) {
-      constexpr int e = decltype(ec)::value;
-      const unsigned o = unsigned(o0 + G::elem_part(P - 1, e) - int(o_lo));
-      vmask |= (o < span ? 1u : 0u) << e;
-    });
+    // owned outputs o in [o_lo, o_hi) of the segment starting at g (clipped
+    // to this call's range) -> writeback mask (item-invariant): element e of
+    // this thread is output o = o0 + elem_part(e), kept iff o_lo <= o < o_hi
+    auto seg_mask = [&](long long g, long long& olo, unsigned& sp) {
+      olo = a.g_lo > g ? a.g_lo - g : 0;
+      const long long ohi = a.g_hi - g < a.seg_len ? a.g_hi - g : a.seg_len;
+      sp = (!live || (a.dbg & 1) || ohi <= olo) ? 0u : unsigned(ohi - olo);
+      unsigned m = 0;
+      sfor<0, E>([&](auto ec) {
+        constexpr int e = decltype(ec)::value;
+        const unsigned o = unsigned(o0 + G::elem_part(P - 1, e) - int(olo));
+        m |= (o < sp ? 1u : 0u) << e;
+      });
+      return m;
+    };
+    long long o_lo, o_lo_b = 0;
+    unsigned span, span_b = 0;
+    const unsigned vmask = seg_mask(g0, o_lo, span);
+    const unsigned vmask_b =
+        MODE == FMODE_R2R ? seg_mask(g0 + a.seg_len, o_lo_b, span_b) : 0u;
+    const long long w0 = g0 - a.t0 + a.origin;
     const int f_lo = fc * a.fchunk;
     const int f_hi = min(a.n_fil, f_lo + a.fchunk);
     const long long nit = it + gridDim.x;
@@ -678,7 +718,27 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     // ---- segment staging: zero-extended window, top-window layout
     // (_gather, _kernels_nb.py:206-215)
     Cpx<R> x[E];
-    {
+    if constexpr (MODE == FMODE_R2R) {
+      // re <- segment 2s's window, im <- segment 2s + 1's.  Both halves are
+      // always loaded (the partner's samples change the rounding of the
+      // other half), so results are bit-identical for any split of the
+      // output range; the caller provides the pair-aligned input extent
+      // (olsb_input_extent_r2r)
+      constexpr int q = P - 1;
+      const long long pa = w0 + G::thread_part(q, t);
+      const long long pbb = pa + a.seg_len;
+      const bool la = live, lb = live;
+      sfor<0, E>([&](auto ec) {
+        constexpr int e = decltype(ec)::value;
+        const long long ga = pa + G::elem_part(q, e);
+        const long long gb = pbb + G::elem_part(q, e);
+        const R ra = (la && (unsigned long long)ga < (unsigned long long)a.n_s)
+                         ? a.xr[ga - a.x_base] : R(0);
+        const R rb = (lb && (unsigned long long)gb < (unsigned long long)a.n_s)
+                         ? a.xr[gb - a.x_base] : R(0);
+        x[e] = Cpx<R>{ra, rb};
+      });
+    } else {
       constexpr int q = P - 1;
       const long long pb = w0 + G::thread_part(q, t);
       const Cpx<R>* xp = a.x + (pb - a.x_base);
@@ -804,13 +864,33 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
       // in-place sample p is output o = p - t0 of this segment, kept iff
       // o_lo <= o < o_hi.  With the 32-aligned engine grid every warp store
       // covers one aligned 256-byte chunk of the output row.
-      {
+      if constexpr (MODE == FMODE_C2C) {
         const long long goff = (long long)f * a.out_ld + (g0 - a.out_base);
         Cpx<R>* orow = a.out + goff + o0;
         sfor<0, E>([&](auto ec) {
           constexpr int e = decltype(ec)::value;
           constexpr int pe = G::elem_part(P - 1, e);
           st_cs_mask<(1u << e)>(orow + pe, y[e], vmask);
+        });
+      } else {
+        // real outputs: |y|^2 (ABS2), or re -> segment 2s and im -> 2s + 1
+        // (R2R, squared for magnitude_squared as fused_r2r pp_kind 2)
+        const long long goff = (long long)f * a.out_ld + (g0 - a.out_base);
+        R* orow = a.outr + goff + o0;
+        const bool sq = a.pp_kind == OLSB_PP_MAG2;
+        sfor<0, E>([&](auto ec) {
+          constexpr int e = decltype(ec)::value;
+          constexpr int pe = G::elem_part(P - 1, e);
+          if constexpr (MODE == FMODE_ABS2) {
+            st_cs_mask_r<(1u << e)>(orow + pe,
+                                    fmaR(y[e].re, y[e].re, y[e].im * y[e].im),
+                                    vmask);
+          } else {
+            const R va = sq ? y[e].re * y[e].re : y[e].re;
+            const R vb = sq ? y[e].im * y[e].im : y[e].im;
+            st_cs_mask_r<(1u << e)>(orow + pe, va, vmask);
+            st_cs_mask_r<(1u << e)>(orow + a.seg_len + pe, vb, vmask_b);
+          }
         });
       }
     }

@@ -229,15 +229,18 @@ static void engine_grid(int n, int t0, long long l_eff, int* t0e,
   }
 }
 
-static int fused_range(const void* x, int64_t x_base, int64_t n_s,
+// mode: FMODE_C2C (complex x / out), FMODE_R2R (real x / out, segment
+// pairs), FMODE_ABS2 (complex x, real |y|^2 out)
+static int fused_range(int mode, const void* x, int64_t x_base, int64_t n_s,
                        const void* spectra_dev, int n_fil, int n, int t0,
                        int origin, int64_t l_eff, int64_t g_lo, int64_t g_hi,
                        int pp_kind, double pp_c, void* out, int64_t out_ld,
                        int64_t out_base, int precision, void* stream) {
   const int logn = log2_of(n);
   if (logn < 0) return OLSB_E_BAD_LENGTH;
-  if (pp_kind != OLSB_PP_NONE && pp_kind != OLSB_PP_SCALE)
-    return OLSB_E_UNSUPPORTED;
+  const bool pp_ok = pp_kind == OLSB_PP_NONE || pp_kind == OLSB_PP_SCALE ||
+                     (mode == FMODE_R2R && pp_kind == OLSB_PP_MAG2);
+  if (!pp_ok) return OLSB_E_UNSUPPORTED;
   if (n_s < 1 || n_fil < 0 || g_lo < 0 || g_hi < g_lo) return OLSB_E_BAD_ARG;
   if (l_eff < 1 || t0 < 0 || t0 + l_eff > n) return OLSB_E_GEOMETRY;
   if (g_hi > n_s) g_hi = n_s;
@@ -251,6 +254,7 @@ static int fused_range(const void* x, int64_t x_base, int64_t n_s,
     return dispatch_n<R>(logn, [&](auto lc) {
       FusedArgs<R> a = {};
       a.x = static_cast<const Cpx<R>*>(x);
+      a.xr = static_cast<const R*>(x);
       a.x_base = x_base;
       a.n_s = n_s;
       a.spec = static_cast<const typename V16<R>::type*>(spectra_dev);
@@ -262,17 +266,33 @@ static int fused_range(const void* x, int64_t x_base, int64_t n_s,
       a.seg_len = le;
       a.k_lo = g_lo / le;
       a.k_hi = (g_hi + le - 1) / le;
+      if (mode == FMODE_R2R) {  // segment pairs {2k, 2k + 1}
+        a.k_lo /= 2;
+        a.k_hi = (a.k_hi + 1) / 2;
+      }
       a.g_lo = g_lo;
       a.g_hi = g_hi;
       a.pp_c = R(pp_c);
       a.out = static_cast<Cpx<R>*>(out);
+      a.outr = static_cast<R*>(out);
       a.out_ld = out_ld;
       a.out_base = out_base;
       a.dbg = debug_env();
       return launch_fused<R, decltype(lc)::value>(
-          a, static_cast<cudaStream_t>(stream));
+          a, mode, static_cast<cudaStream_t>(stream));
     });
   });
+}
+
+static int check_ref_geometry(int64_t n_s, int n_fil, int n, int m, int origin,
+                              int64_t l_eff, int t0, int64_t win_off,
+                              int64_t seg_lo, int64_t seg_hi) {
+  if (n_s < 1 || n_fil < 0 || m < 1 || m > n || origin < 0 || origin >= m ||
+      seg_lo < 0 || seg_hi < seg_lo)
+    return OLSB_E_BAD_ARG;
+  if (l_eff < 1 || t0 < 0 || t0 + l_eff > n || win_off != origin - t0)
+    return OLSB_E_GEOMETRY;
+  return 0;
 }
 
 int olsb_fused_c2c(const void* x, int64_t x_base, int64_t n_s,
@@ -281,16 +301,45 @@ int olsb_fused_c2c(const void* x, int64_t x_base, int64_t n_s,
                    int64_t seg_lo, int64_t seg_hi, int pp_kind, double pp_c,
                    void* out, int64_t out_ld, int64_t out_base,
                    int precision, void* stream) {
-  if (n_s < 1 || n_fil < 0 || m < 1 || m > n || origin < 0 || origin >= m ||
-      seg_lo < 0 || seg_hi < seg_lo)
-    return OLSB_E_BAD_ARG;
-  if (l_eff < 1 || t0 < 0 || t0 + l_eff > n || win_off != origin - t0)
-    return OLSB_E_GEOMETRY;
+  const int rc = check_ref_geometry(n_s, n_fil, n, m, origin, l_eff, t0,
+                                    win_off, seg_lo, seg_hi);
+  if (rc) return rc;
   // the reference segments [seg_lo, seg_hi) own outputs
   // [seg_lo * l_eff, min(seg_hi * l_eff, n_s))
-  return fused_range(x, x_base, n_s, spectra_dev, n_fil, n, t0, origin, l_eff,
-                     seg_lo * l_eff, std::min<int64_t>(seg_hi * l_eff, n_s),
-                     pp_kind, pp_c, out, out_ld, out_base, precision, stream);
+  return fused_range(FMODE_C2C, x, x_base, n_s, spectra_dev, n_fil, n, t0,
+                     origin, l_eff, seg_lo * l_eff,
+                     std::min<int64_t>(seg_hi * l_eff, n_s), pp_kind, pp_c,
+                     out, out_ld, out_base, precision, stream);
+}
+
+int olsb_fused_c2c_abs2(const void* x, int64_t x_base, int64_t n_s,
+                        const void* spectra_dev, int n_fil, int n, int m,
+                        int origin, int64_t l_eff, int t0, int64_t win_off,
+                        int64_t seg_lo, int64_t seg_hi, void* out,
+                        int64_t out_ld, int64_t out_base, int precision,
+                        void* stream) {
+  const int rc = check_ref_geometry(n_s, n_fil, n, m, origin, l_eff, t0,
+                                    win_off, seg_lo, seg_hi);
+  if (rc) return rc;
+  return fused_range(FMODE_ABS2, x, x_base, n_s, spectra_dev, n_fil, n, t0,
+                     origin, l_eff, seg_lo * l_eff,
+                     std::min<int64_t>(seg_hi * l_eff, n_s), OLSB_PP_NONE, 1.0,
+                     out, out_ld, out_base, precision, stream);
+}
+
+int olsb_fused_r2r(const void* x, int64_t x_base, int64_t n_s,
+                   const void* spectra_dev, int n_fil, int n, int m,
+                   int origin, int64_t l_eff, int t0, int64_t win_off,
+                   int64_t seg_lo, int64_t seg_hi, int pp_kind, double pp_c,
+                   void* out, int64_t out_ld, int64_t out_base,
+                   int precision, void* stream) {
+  const int rc = check_ref_geometry(n_s, n_fil, n, m, origin, l_eff, t0,
+                                    win_off, seg_lo, seg_hi);
+  if (rc) return rc;
+  return fused_range(FMODE_R2R, x, x_base, n_s, spectra_dev, n_fil, n, t0,
+                     origin, l_eff, seg_lo * l_eff,
+                     std::min<int64_t>(seg_hi * l_eff, n_s), pp_kind, pp_c,
+                     out, out_ld, out_base, precision, stream);
 }
 
 int olsb_fused_c2c_range(const void* x, int64_t x_base, int64_t n_s,
@@ -299,13 +348,24 @@ int olsb_fused_c2c_range(const void* x, int64_t x_base, int64_t n_s,
                          double pp_c, void* out, int64_t out_ld,
                          int64_t out_base, int precision, void* stream) {
   if (m < 1 || m > n || origin < 0 || origin >= m) return OLSB_E_BAD_ARG;
-  return fused_range(x, x_base, n_s, spectra_dev, n_fil, n, m - 1, origin,
-                     n - m + 1, g_lo, g_hi, pp_kind, pp_c, out, out_ld,
+  return fused_range(FMODE_C2C, x, x_base, n_s, spectra_dev, n_fil, n, m - 1,
+                     origin, n - m + 1, g_lo, g_hi, pp_kind, pp_c, out, out_ld,
                      out_base, precision, stream);
 }
 
-int olsb_input_extent(int n, int m, int origin, int64_t g_lo, int64_t g_hi,
-                      int64_t* x_lo, int64_t* x_hi) {
+int olsb_fused_r2r_range(const void* x, int64_t x_base, int64_t n_s,
+                         const void* spectra_dev, int n_fil, int n, int m,
+                         int origin, int64_t g_lo, int64_t g_hi, int pp_kind,
+                         double pp_c, void* out, int64_t out_ld,
+                         int64_t out_base, int precision, void* stream) {
+  if (m < 1 || m > n || origin < 0 || origin >= m) return OLSB_E_BAD_ARG;
+  return fused_range(FMODE_R2R, x, x_base, n_s, spectra_dev, n_fil, n, m - 1,
+                     origin, n - m + 1, g_lo, g_hi, pp_kind, pp_c, out, out_ld,
+                     out_base, precision, stream);
+}
+
+static int input_extent(int mode, int n, int m, int origin, int64_t g_lo,
+                        int64_t g_hi, int64_t* x_lo, int64_t* x_hi) {
   if (log2_of(n) < 0) return OLSB_E_BAD_LENGTH;
   if (m < 1 || m > n || origin < 0 || origin >= m || g_hi < g_lo || !x_lo ||
       !x_hi)
@@ -313,10 +373,24 @@ int olsb_input_extent(int n, int m, int origin, int64_t g_lo, int64_t g_hi,
   int t0e;
   long long le;
   engine_grid(n, m - 1, n - m + 1, &t0e, &le);
-  const long long k_lo = g_lo / le, k_hi = (g_hi + le - 1) / le;
+  long long k_lo = g_lo / le, k_hi = (g_hi + le - 1) / le;
+  if (mode == FMODE_R2R) {  // whole segment pairs {2k, 2k + 1}
+    k_lo = (k_lo / 2) * 2;
+    k_hi = ((k_hi + 1) / 2) * 2;
+  }
   *x_lo = k_lo * le - t0e + origin;
   *x_hi = (k_hi - 1) * le - t0e + origin + n;
   return 0;
+}
+
+int olsb_input_extent(int n, int m, int origin, int64_t g_lo, int64_t g_hi,
+                      int64_t* x_lo, int64_t* x_hi) {
+  return input_extent(FMODE_C2C, n, m, origin, g_lo, g_hi, x_lo, x_hi);
+}
+
+int olsb_input_extent_r2r(int n, int m, int origin, int64_t g_lo,
+                          int64_t g_hi, int64_t* x_lo, int64_t* x_hi) {
+  return input_extent(FMODE_R2R, n, m, origin, g_lo, g_hi, x_lo, x_hi);
 }
 
 int olsb_copy2d_async(void* dst, int64_t dst_pitch_bytes, const void* src,

@@ -67,11 +67,9 @@ template <int LOGN, int V>
 struct Variant {
   static constexpr int T = Geo<LOGN>::T;
   // {SEGS, NBUF, HM, BAR, MINB (warpgroups/SM), MIDREG, TMX, PREF}
-  static constexpr int tab[8][8] = {
+  static constexpr int tab[4][8] = {
       {1, 1, H_TEX, 0, 4, 0, 0, 0}, {1, 1, H_TEX, 0, 4, 0, 1, 1},
-      {1, 1, H_TEX, 0, 4, 0, 2, 1}, {1, 2, H_TEX, 0, 4, 0, 2, 1},
-      {1, 1, H_TEX, 0, 5, 0, 1, 0}, {1, 2, H_TEX, 0, 4, 0, 1, 1},
-      {2, 1, H_TEX, 1, 4, 0, 2, 1}, {2, 1, H_TEX, 0, 4, 0, 2, 1}};
+      {1, 1, H_TEX, 0, 4, 0, 2, 1}, {1, 2, H_TEX, 0, 4, 0, 2, 1}};
   static constexpr int segs = tab[V][0] * std::max(1, 128 / T);
   static constexpr int minb = std::max(1, tab[V][4] * 128 / (segs * T));
   using type = KCfg<float, LOGN, segs, tab[V][1], tab[V][2], tab[V][3], minb,
@@ -94,9 +92,9 @@ inline int variant_env() {
   return v;
 }
 
-template <class C>
+template <class C, int MODE = FMODE_C2C>
 int launch_fused_cfg(FusedArgs<typename C::R> a, cudaStream_t st) {
-  auto kern = fused_c2c_kernel<C>;
+  auto kern = fused_c2c_kernel<C, MODE>;
   int resident = 0;
   int rc = prepare(kern, C::f_smem_bytes, C::THREADS, &resident);
   if (rc) return rc;
@@ -119,21 +117,20 @@ int launch_fused_cfg(FusedArgs<typename C::R> a, cudaStream_t st) {
 }
 
 template <class R, int LOGN>
-int launch_fused(FusedArgs<R> a, cudaStream_t st) {
+int launch_fused(FusedArgs<R> a, int mode, cudaStream_t st) {
+  using D = typename DefaultPolicy<R, LOGN>::type;
+  if (mode == FMODE_R2R) return launch_fused_cfg<D, FMODE_R2R>(a, st);
+  if (mode == FMODE_ABS2) return launch_fused_cfg<D, FMODE_ABS2>(a, st);
   if constexpr (std::is_same<R, float>::value) {
     switch (variant_env()) {
       case 0: return launch_fused_cfg<typename Variant<LOGN, 0>::type>(a, st);
       case 1: return launch_fused_cfg<typename Variant<LOGN, 1>::type>(a, st);
       case 2: return launch_fused_cfg<typename Variant<LOGN, 2>::type>(a, st);
       case 3: return launch_fused_cfg<typename Variant<LOGN, 3>::type>(a, st);
-      case 4: return launch_fused_cfg<typename Variant<LOGN, 4>::type>(a, st);
-      case 5: return launch_fused_cfg<typename Variant<LOGN, 5>::type>(a, st);
-      case 6: return launch_fused_cfg<typename Variant<LOGN, 6>::type>(a, st);
-      case 7: return launch_fused_cfg<typename Variant<LOGN, 7>::type>(a, st);
       default: break;
     }
   }
-  return launch_fused_cfg<typename DefaultPolicy<R, LOGN>::type>(a, st);
+  return launch_fused_cfg<D>(a, st);
 }
 
 template <class R, int LOGN>
@@ -179,7 +176,8 @@ int launch_perm_to_dev(const Cpx<R>* perm, void* dev, int rows,
 }  // namespace olsb
 
 #define OLSB_LAUNCHERS(EXT, R, L)                                            \
-  EXT template int olsb::launch_fused<R, L>(olsb::FusedArgs<R>, cudaStream_t); \
+  EXT template int olsb::launch_fused<R, L>(olsb::FusedArgs<R>, int,         \
+                                            cudaStream_t);                 \
   EXT template int olsb::launch_fwd_rows<R, L>(olsb::RowsArgs<R>,             \
                                                cudaStream_t);                 \
   EXT template int olsb::launch_inv_rows<R, L>(                               \

@@ -187,7 +187,17 @@ def transform_filters(filters: FilterSet, seg_plan: SegmentPlan,
                              device=taps.device)
         padded[:, :filters.tap_length] = taps
         spectra = torch.fft.rfft(padded, dim=1)
-        return filters.with_spectra(spectra, layout, n)
+        # the fused real engine transforms two real segments as one complex
+        # one, so it multiplies by the full complex spectrum of the real taps
+        # (engine layout, same in-register FFT as the c2c path)
+        ctaps = taps.to(precision.torch_complex).contiguous()
+        dev = torch.empty((filters.n_filters, n), dtype=precision.torch_complex,
+                          device=taps.device)
+        with torch.cuda.device(taps.device):
+            _lib.call("olsb_filter_spectra_c2c", ctaps.data_ptr(),
+                      filters.n_filters, filters.tap_length, n, None,
+                      dev.data_ptr(), precision.code, _stream_ptr())
+        return filters.with_spectra(spectra, layout, n, dev)
     ctaps = taps.to(precision.torch_complex).contiguous()
     if layout == "permuted":
         spectra = torch.empty((filters.n_filters, n),
@@ -210,6 +220,20 @@ def _engine_spectra(filters: FilterSet) -> torch.Tensor:
     filled elsewhere (e.g. handed over from the reference)."""
     if filters.spectra_dev is not None:
         return filters.spectra_dev
+    if filters.spectra.shape[1] != filters.spectra_n:
+        # packed real (rfft) spectra: the engine needs the full complex
+        # spectrum of the real taps, recomputed by the engine's own FFT
+        n = filters.spectra_n
+        prec = (Precision.single if filters.taps.dtype == torch.float32
+                else Precision.double)
+        ctaps = filters.taps.to(prec.torch_complex).contiguous()
+        dev = torch.empty((filters.n_filters, n), dtype=prec.torch_complex,
+                          device=ctaps.device)
+        _lib.call("olsb_filter_spectra_c2c", ctaps.data_ptr(),
+                  filters.n_filters, filters.tap_length, n, None,
+                  dev.data_ptr(), prec.code, _stream_ptr())
+        object.__setattr__(filters, "spectra_dev", dev)
+        return dev
     spec = filters.spectra.contiguous()
     dev = torch.empty_like(spec)
     prec = Precision.single if spec.dtype == torch.complex64 else Precision.double
@@ -302,10 +326,13 @@ def convolve(signal: Signal, filters: FilterSet, seg_plan: SegmentPlan,
                            device=signal.samples.device)
 
     l_eff, t0, win_off, n_seg_eff = _geometry(seg_plan, pp.halo)
-    if seg_plan.mode == "r2r" or pp.kind not in ("none", "scale"):
+    if pp.kind == "derivative":
         raise EngineError(
-            f"mode {seg_plan.mode!r} with postproc {pp.kind!r} is not in this "
-            "build's fused engine (SURVEY §8(f) rows 2-3)")
+            "postproc 'derivative' (non-local epilogue) is not in this build's "
+            "engine (SURVEY §8(f) row 3)")
+    if seg_plan.mode == "r2r" and pp.kind not in ("none", "scale",
+                                                  "magnitude_squared"):
+        raise EngineError(f"r2r with postproc {pp.kind!r} is not supported")
     if out is not None:
         if tuple(out.shape) != (n_fil, n_s) or out.dtype != out_dtype:
             raise ValueError(f"out must be {(n_fil, n_s)} {out_dtype}")
@@ -334,6 +361,17 @@ def convolve(signal: Signal, filters: FilterSet, seg_plan: SegmentPlan,
                       win_off, n_seg_eff, out)
 
 
+def _engine_entry(seg_plan: SegmentPlan, pp: PostProcSpec) -> str:
+    """C-ABI entry of the fused engine for a plan + post-process: the
+    reference's K.fused_c2c / K.fused_c2c_abs2 / K.fused_r2r
+    (_kernels_nb.py:265-337)."""
+    if seg_plan.mode == "r2r":
+        return "olsb_fused_r2r"
+    if pp.kind == "magnitude_squared":
+        return "olsb_fused_c2c_abs2"
+    return "olsb_fused_c2c"
+
+
 def fused_launch(x: torch.Tensor, x_base: int, n_s: int,
                  spec_dev: torch.Tensor, n_fil: int, seg_plan: SegmentPlan,
                  l_eff: int, t0: int, win_off: int, seg_lo: int, seg_hi: int,
@@ -341,12 +379,18 @@ def fused_launch(x: torch.Tensor, x_base: int, n_s: int,
                  out_base: int, precision: Precision,
                  stream: Optional[int] = None) -> None:
     """One call of the C-ABI fused kernel (the reference's K.fused_c2c,
-    _kernels_nb.py:265-285) on the current stream."""
-    _lib.call("olsb_fused_c2c", x.data_ptr(), x_base, n_s, spec_dev.data_ptr(),
-              n_fil, seg_plan.fft_len, seg_plan.tap_len, seg_plan.origin,
-              l_eff, t0, win_off, seg_lo, seg_hi, pp.code, float(pp.scale),
-              out.data_ptr(), out_ld, out_base, precision.code,
-              _stream_ptr() if stream is None else stream)
+    K.fused_c2c_abs2 or K.fused_r2r, _kernels_nb.py:265-337) on the current
+    stream."""
+    entry = _engine_entry(seg_plan, pp)
+    common = (x.data_ptr(), x_base, n_s, spec_dev.data_ptr(), n_fil,
+              seg_plan.fft_len, seg_plan.tap_len, seg_plan.origin, l_eff, t0,
+              win_off, seg_lo, seg_hi)
+    tail = (out.data_ptr(), out_ld, out_base, precision.code,
+            _stream_ptr() if stream is None else stream)
+    if entry == "olsb_fused_c2c_abs2":
+        _lib.call(entry, *common, *tail)
+    else:
+        _lib.call(entry, *common, pp.code, float(pp.scale), *tail)
 
 
 def fused_range_launch(x: torch.Tensor, x_base: int, n_s: int,
@@ -355,12 +399,18 @@ def fused_range_launch(x: torch.Tensor, x_base: int, n_s: int,
                        pp: PostProcSpec, out: torch.Tensor, out_ld: int,
                        out_base: int, precision: Precision,
                        stream: Optional[int] = None) -> None:
-    """Outputs [g_lo, g_hi) through olsb_fused_c2c_range (shards, streams)."""
-    _lib.call("olsb_fused_c2c_range", x.data_ptr(), x_base, n_s,
-              spec_dev.data_ptr(), n_fil, seg_plan.fft_len, seg_plan.tap_len,
-              seg_plan.origin, g_lo, g_hi, pp.code, float(pp.scale),
-              out.data_ptr(), out_ld, out_base, precision.code,
-              _stream_ptr() if stream is None else stream)
+    """Outputs [g_lo, g_hi) through olsb_fused_{c2c,r2r}_range (shards,
+    streams)."""
+    entry = ("olsb_fused_r2r_range" if seg_plan.mode == "r2r"
+             else "olsb_fused_c2c_range")
+    if pp.kind not in ("none", "scale") and not (
+            seg_plan.mode == "r2r" and pp.kind == "magnitude_squared"):
+        raise EngineError(f"range launches support postproc none|scale "
+                          f"(r2r: also magnitude_squared), got {pp.kind!r}")
+    _lib.call(entry, x.data_ptr(), x_base, n_s, spec_dev.data_ptr(), n_fil,
+              seg_plan.fft_len, seg_plan.tap_len, seg_plan.origin, g_lo, g_hi,
+              pp.code, float(pp.scale), out.data_ptr(), out_ld, out_base,
+              precision.code, _stream_ptr() if stream is None else stream)
 
 
 def input_extent(seg_plan: SegmentPlan, g_lo: int, g_hi: int) -> Tuple[int, int]:
@@ -368,9 +418,11 @@ def input_extent(seg_plan: SegmentPlan, g_lo: int, g_hi: int) -> Tuple[int, int]
     [g_lo, g_hi) (its shard plus halos; clip to [0, n_s) before copying)."""
     import ctypes
     lo, hi = ctypes.c_int64(), ctypes.c_int64()
-    _lib.check(_lib.load().olsb_input_extent(
+    fn = ("olsb_input_extent_r2r" if seg_plan.mode == "r2r"
+          else "olsb_input_extent")
+    _lib.check(getattr(_lib.load(), fn)(
         seg_plan.fft_len, seg_plan.tap_len, seg_plan.origin, g_lo, g_hi,
-        ctypes.byref(lo), ctypes.byref(hi)), "olsb_input_extent")
+        ctypes.byref(lo), ctypes.byref(hi)), fn)
     return lo.value, hi.value
 
 
@@ -428,20 +480,24 @@ def _fused_streaming(signal, spec_dev, seg_plan, pp, precision, l_eff, t0,
 def _pipelined(signal, filters, seg_plan, pp, precision, l_eff, t0, win_off,
                n_seg, out):
     """cuFFT-based OLS, the paper's comparison point (Algorithm 1;
-    reference _pipelined ols.py:363-410): gather -> batched C2C forward ->
-    materialized product -> batched C2C inverse -> discard + store.  Chunked
-    so the (n_fil, rows, n) product stays within PIPELINED_BUDGET_BYTES."""
+    reference _pipelined ols.py:363-410): gather -> batched forward FFT (C2C,
+    or R2C on the real path) -> materialized product -> batched inverse (C2C /
+    C2R) -> discard + store.  Chunked so the (n_fil, rows, n) product stays
+    within PIPELINED_BUDGET_BYTES."""
     n = seg_plan.fft_len
     n_s = signal.length
     x = signal.samples
-    spectra = filters.spectra  # natural order
+    spectra = filters.spectra  # natural order (rfft bins on the real path)
     n_fil = filters.n_filters
     dev = x.device
+    real = seg_plan.mode == "r2r"
+    real_out = real or pp.real_output
     if out is None:
-        out = torch.empty((n_fil, n_s), dtype=precision.torch_complex,
+        out = torch.empty((n_fil, n_s), dtype=(precision.torch_real if real_out
+                                               else precision.torch_complex),
                           device=dev)
-    esize = out.element_size()
-    rows_per = max(1, PIPELINED_BUDGET_BYTES // (2 * n_fil * n * esize))
+    csize = 8 if precision == Precision.single else 16
+    rows_per = max(1, PIPELINED_BUDGET_BYTES // (2 * n_fil * n * csize))
     ar = torch.arange(n, device=dev)
     for lo in range(0, n_seg, rows_per):
         hi = min(lo + rows_per, n_seg)
@@ -450,14 +506,22 @@ def _pipelined(signal, filters, seg_plan, pp, precision, l_eff, t0, win_off,
         ok = (idx >= 0) & (idx < n_s)
         mat = torch.where(ok, x[idx.clamp(0, n_s - 1)],
                           torch.zeros((), dtype=x.dtype, device=dev))
-        fmat = torch.fft.fft(mat, dim=1)
-        mid = torch.fft.ifft(fmat[None, :, :] * spectra[:, None, :], dim=2)
+        if real:
+            fmat = torch.fft.rfft(mat, dim=1)
+            mid = torch.fft.irfft(fmat[None, :, :] * spectra[:, None, :], n=n,
+                                  dim=2)
+        else:
+            fmat = torch.fft.fft(mat, dim=1)
+            mid = torch.fft.ifft(fmat[None, :, :] * spectra[:, None, :], dim=2)
         valid = mid[:, :, t0:t0 + l_eff].reshape(n_fil, -1)
         g_lo = lo * l_eff
         g_hi = min(hi * l_eff, n_s)
         seg_out = valid[:, :g_hi - g_lo]
         if pp.kind == "scale":
             seg_out = seg_out * pp.scale
+        elif pp.kind == "magnitude_squared":
+            seg_out = (seg_out * seg_out if real else
+                       seg_out.real * seg_out.real + seg_out.imag * seg_out.imag)
         out[:, g_lo:g_hi] = seg_out
     return out
 
@@ -466,8 +530,9 @@ def _direct(signal: Signal, filters: FilterSet, pp: PostProcSpec):
     """Direct time-domain convolution on the GPU, float64 accumulate, rounded
     to the signal's precision (oracle.py:20-41): y[f,n] = sum_k h[f,k]
     x[n-k+o], zeros off the ends.  Complex conv = 4 real conv1d calls."""
-    if pp.kind not in ("none", "scale"):
-        raise EngineError("direct_oracle supports postproc none|scale only")
+    if pp.kind == "derivative":
+        raise EngineError("direct_oracle does not support 'derivative'")
+    real = signal.value_kind == "real" and filters.value_kind == "real"
     x = signal.samples.to(torch.complex128)
     h = filters.taps.to(torch.complex128)
     m = filters.tap_length
@@ -486,6 +551,14 @@ def _direct(signal: Signal, filters: FilterSet, pp: PostProcSpec):
     y = torch.complex(yr, yi)[:, :n_s]
     if pp.kind == "scale":
         y = y * pp.scale
+    if real:
+        y = y.real
+        if pp.kind == "magnitude_squared":
+            y = y * y
+        return y.to(signal.precision.torch_real)
+    if pp.kind == "magnitude_squared":
+        return (y.real * y.real + y.imag * y.imag).to(
+            signal.precision.torch_real)
     return y.to(signal.precision.torch_complex)
 
 

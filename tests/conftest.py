@@ -52,6 +52,7 @@ def golden():
         "spectra": np.load(os.path.join(GOLDEN, "spectra.npz")),
         "conv": np.load(os.path.join(GOLDEN, "conv_cases.npz")),
         "cfg": np.load(os.path.join(GOLDEN, "cfg_windows.npz")),
+        "pp": np.load(os.path.join(GOLDEN, "pp_cases.npz")),
     }
 
 

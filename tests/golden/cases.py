@@ -57,6 +57,38 @@ def conv_case_inputs(i):
     return x, taps
 
 
+# real path + post-processing cells:
+# (n_s, m, nfil, n, origin, mode, postproc)
+PP_GRID = [
+    (1, 5, 2, 64, 2, "r2r", "none"),          # single sample
+    (63, 5, 2, 64, 2, "r2r", "none"),
+    (65, 5, 2, 64, 4, "r2r", "scale"),
+    (1000, 1, 3, 8, 0, "r2r", "none"),        # M = 1, N = 8 (r2r floor)
+    (777, 64, 1, 64, 0, "r2r", "none"),       # M = N
+    (5000, 33, 2, 128, 16, "r2r", "none"),
+    (5000, 257, 2, 1024, 128, "r2r", "magnitude_squared"),
+    (9000, 400, 3, 2048, 0, "r2r", "none"),   # FDAS shape, small
+    (9000, 129, 2, 2048, 64, "r2r", "scale"),
+    (12000, 1025, 1, 4096, 512, "r2r", "none"),
+    (10000, 33, 2, 256, 0, "r2r", "none"),
+    (6000, 65, 3, 512, 32, "c2c", "magnitude_squared"),
+    (9000, 400, 2, 2048, 0, "c2c", "magnitude_squared"),
+    (3000, 9, 2, 16, 8, "c2c", "magnitude_squared"),
+]
+
+
+def pp_case_inputs(i):
+    ns, m, nfil, n, origin, mode, pp = PP_GRID[i]
+    rng = np.random.default_rng([40, i, ns, m, nfil, n, origin])
+    if mode == "r2r":
+        return rng.standard_normal(ns), rng.standard_normal((nfil, m))
+    x = rng.standard_normal(ns) + 1j * rng.standard_normal(ns)
+    taps = rng.standard_normal((nfil, m)) + 1j * rng.standard_normal((nfil, m))
+    return x, taps
+
+
+PP_SCALE = 0.75
+
 # BASELINE.json configs 1-4 (SURVEY §8 geometry table); cfg5 (2^30) cannot
 # run on the reference and is checked by windows against the oracle instead.
 CFGS = [

@@ -16,6 +16,8 @@ spectra.npz        transform_filters(..., "permuted") (ols.py:168-205).
 conv_cases.npz     convolve(variant="fused") c2c (ols.py:257-360) on a grid of
                    small cells incl. every edge case of SURVEY §8(a): first /
                    last segment, M=1, M=N, N_s < L, origin > 0, real taps.
+pp_cases.npz       the real (r2r) path and the magnitude_squared epilogue
+                   (fused_r2r / fused_c2c_abs2) on a grid of small cells.
 cfg_windows.npz    BASELINE.json configs 1-4 at FULL size: float64 reference
                    output on fixed windows + per-filter checksums.  Inputs are
                    regenerated anywhere from the reference's own generator
@@ -38,8 +40,9 @@ sys.path.insert(0, "/root/reference/pkg/src")
 import olsconv as oc  # noqa: E402  (the reference)
 
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
-from cases import (CFGS, CONV_GRID, WIN, conv_case_inputs,  # noqa: E402
-                   gen_inputs, window_starts)
+from cases import (CFGS, CONV_GRID, PP_GRID, PP_SCALE, WIN,  # noqa: E402
+                   conv_case_inputs, gen_inputs, pp_case_inputs,
+                   window_starts)
 from olsconv import Precision  # noqa: E402
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -99,6 +102,25 @@ def conv_fixtures():
     np.savez_compressed(os.path.join(HERE, "conv_cases.npz"), **out)
 
 
+def pp_fixtures():
+    """Real path (fused_r2r, _kernels_nb.py:312-337) and magnitude_squared
+    (fused_c2c_abs2, :288-309) through the reference's convolve."""
+    out = {}
+    for i, (ns, m, nfil, n, origin, mode, ppk) in enumerate(PP_GRID):
+        x, taps = pp_case_inputs(i)
+        p = oc.plan(ns, m, mode, origin, n)
+        pp = oc.PostProcSpec(ppk, PP_SCALE if ppk == "scale" else 1.0)
+        vk = "real" if mode == "r2r" else "complex"
+        for prec in Precision:
+            sig = oc.make_signal(x, vk, prec)
+            fs = oc.make_filterset(taps, origin, prec)
+            y = oc.convolve(sig, fs, p, variant="fused", postproc=pp,
+                            workers=1)
+            assert np.all(np.isfinite(y))
+            out[f"y_{prec.value}_{i}"] = y
+    np.savez_compressed(os.path.join(HERE, "pp_cases.npz"), **out)
+
+
 def cfg_fixtures():
     out = {}
     for name, ns, m, nfil, n in CFGS:
@@ -121,13 +143,15 @@ def cfg_fixtures():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["fft", "spectra", "conv", "cfg"]
+    which = sys.argv[1:] or ["fft", "spectra", "conv", "pp", "cfg"]
     if "fft" in which:
         fft_fixtures()
     if "spectra" in which:
         spectra_fixtures()
     if "conv" in which:
         conv_fixtures()
+    if "pp" in which:
+        pp_fixtures()
     if "cfg" in which:
         cfg_fixtures()
     print("backend:", oc.backend_name())

@@ -1,0 +1,118 @@
+"""GPU parity of the real (r2r) fused path and the magnitude_squared
+epilogue against the reference's own outputs
+(tests/golden/pp_cases.npz, made by the reference's fused_r2r /
+fused_c2c_abs2 and pinned against the oracle in test_oracle.py).
+
+The engine transforms two real segments as one complex segment (re / im), so
+the tests also cover odd segment counts, range splits that start on the
+second segment of a pair, and the host streaming path.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from cases import PP_GRID, PP_SCALE, pp_case_inputs
+from conftest import rel_err, rel_l2_per_filter
+
+pytestmark = pytest.mark.gpu
+
+L2_TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def oc():
+    import paper_1910_01972_b200 as m
+    assert torch.cuda.is_available()
+    return m
+
+
+def _run(oc, case, prec, out=None, workers=1, layout="natural"):
+    ns, m, nfil, n, origin, mode, ppk = PP_GRID[case]
+    x, taps = pp_case_inputs(case)
+    P = oc.Precision(prec)
+    vk = "real" if mode == "r2r" else "complex"
+    p = oc.plan(ns, m, mode, origin, n)
+    pp = oc.PostProcSpec(ppk, PP_SCALE if ppk == "scale" else 1.0)
+    fs = oc.transform_filters(oc.make_filterset(taps, origin, P), p,
+                              "natural" if mode == "r2r" else "permuted")
+    return oc.convolve(oc.make_signal(x, vk, P), fs, p, postproc=pp, out=out,
+                       workers=workers), p, fs
+
+
+@pytest.mark.parametrize("case", range(len(PP_GRID)))
+def test_real_path_and_abs2_vs_reference(oc, golden, case):
+    ns, m, nfil, n, origin, mode, ppk = PP_GRID[case]
+    ref = golden["pp"][f"y_double_{case}"]
+    for prec in ("single", "double"):
+        P = oc.Precision(prec)
+        out = torch.full((nfil, ns), float("nan"), dtype=P.torch_real,
+                         device="cuda")
+        y, _, _ = _run(oc, case, prec, out=out)
+        y = y.cpu().numpy()
+        assert np.isrealobj(y)
+        assert np.all(np.isfinite(y)), prec   # every output written once
+        tol_l2, tol_inf = (L2_TOL, 1e-4) if prec == "single" else (1e-12, 1e-10)
+        if ppk == "magnitude_squared":      # squares double the relative error
+            tol_l2, tol_inf = 2 * tol_l2, 2 * tol_inf
+        assert rel_l2_per_filter(y, ref) <= tol_l2, prec
+        assert rel_err(y, ref) <= tol_inf, prec
+
+
+def test_r2r_splits_bit_identical(oc):
+    # workers, output-range cuts at odd segment boundaries (second half of a
+    # segment pair) and the host streaming path all give the same bits
+    from paper_1910_01972_b200.ols import fused_range_launch
+    for case in (7, 8, 10):
+        ns, m, nfil, n, origin, mode, ppk = PP_GRID[case]
+        a, p, fs = _run(oc, case, "single")
+        b, _, _ = _run(oc, case, "single", workers=5)
+        assert torch.equal(a, b)
+        x, _ = pp_case_inputs(case)
+        P = oc.Precision.single
+        sig = oc.make_signal(x, "real", P)
+        pp = oc.PostProcSpec(ppk, PP_SCALE if ppk == "scale" else 1.0)
+        le = p.valid_len
+        c = torch.full_like(a, float("nan"))
+        cuts = [0, 1, le + 3, 3 * le, 3 * le + 1, ns // 2, ns - 2, ns]
+        cuts = sorted(set(min(max(v, 0), ns) for v in cuts))
+        for lo, hi in zip(cuts[:-1], cuts[1:]):
+            fused_range_launch(sig.samples, 0, ns, fs.spectra_dev, nfil, p, lo,
+                               hi, pp, c, ns, 0, P)
+        assert torch.equal(a, c)
+        hsig = oc.make_signal(torch.from_numpy(x.astype(np.float32)).pin_memory(),
+                              "real", P, device="cpu")
+        host = torch.empty((nfil, ns), dtype=torch.float32).pin_memory()
+        oc.convolve(hsig, fs, p, postproc=pp, out=host, chunk_segments=3)
+        assert torch.equal(host, a.cpu())
+
+
+def test_r2r_vs_cufft_pipelined_and_direct(oc):
+    # the cuFFT comparison point (R2C / C2R) and the direct oracle variant
+    case = 7
+    a, p, fs = _run(oc, case, "single")
+    ns, m, nfil, n, origin, mode, ppk = PP_GRID[case]
+    x, taps = pp_case_inputs(case)
+    P = oc.Precision.single
+    sig = oc.make_signal(x, "real", P)
+    b = oc.convolve(sig, fs, p, variant="pipelined")
+    d = oc.convolve(sig, oc.make_filterset(taps, origin, P), p,
+                    variant="direct_oracle")
+    assert b.dtype == torch.float32 and d.dtype == torch.float32
+    assert rel_err(a.cpu().numpy(), d.cpu().numpy()) < 1e-5
+    assert rel_err(b.cpu().numpy(), d.cpu().numpy()) < 1e-5
+
+
+def test_fdas_shape_real_full_output_vs_oracle(oc):
+    # cfg3 geometry on the real path at 2^20 samples, every output checked
+    import oracle
+    ns, m, nfil, n = 1 << 20, 400, 8, 2048
+    rng = np.random.default_rng([50, ns, m, nfil])
+    x = rng.standard_normal(ns)
+    taps = rng.standard_normal((nfil, m))
+    P = oc.Precision.single
+    p = oc.plan(ns, m, "r2r", 0, n)
+    fs = oc.transform_filters(oc.make_filterset(taps, 0, P), p, "natural")
+    y = oc.convolve(oc.make_signal(x, "real", P), fs, p).cpu().numpy()
+    ref = oracle.direct_convolve(x, taps, 0).real
+    assert rel_l2_per_filter(y, ref) <= L2_TOL

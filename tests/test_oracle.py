@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import oracle
-from cases import CONV_GRID, conv_case_inputs
+from cases import CONV_GRID, PP_GRID, PP_SCALE, conv_case_inputs, pp_case_inputs
 from conftest import rel_err
 
 
@@ -118,3 +118,25 @@ def test_cfg_golden_windows_consistent(golden):
     assert rel_err(win, g["cfg1_win"]) < 1e-6   # fixture stored as complex64
     assert np.allclose(np.sum(np.abs(y) ** 2, axis=1), g["cfg1_sumsq"],
                        rtol=1e-12)
+
+
+@pytest.mark.parametrize("case", range(len(PP_GRID)))
+def test_pp_fixtures_match_direct_oracle(golden, case):
+    """The reference's real path / magnitude_squared outputs (pp_cases.npz)
+    agree with the oracle's float64 direct convolution (pins the fixtures the
+    GPU r2r / abs2 parity tests use)."""
+    ns, m, nfil, n, origin, mode, ppk = PP_GRID[case]
+    x, taps = pp_case_inputs(case)
+    y = oracle.direct_convolve(x, taps, origin)
+    if ppk == "scale":
+        y = y * PP_SCALE
+    if mode == "r2r":
+        y = y.real
+        if ppk == "magnitude_squared":
+            y = y * y
+    elif ppk == "magnitude_squared":
+        y = np.abs(y) ** 2
+    ref = golden["pp"][f"y_double_{case}"]
+    assert ref.shape == (nfil, ns)
+    assert np.isrealobj(ref) == (mode == "r2r" or ppk == "magnitude_squared")
+    assert rel_err(ref, y) < 1e-10

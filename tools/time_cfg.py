@@ -36,13 +36,18 @@ def parity():
 
 
 def time_cfg(name, reps=20):
-    ns, m, nfil, n = CFG[name]
+    ns, m, nfil, n, *mode = CFG[name]
+    mode = mode[0] if mode else "c2c"
     x, taps = gen_inputs(ns, m, nfil)
     P = ob.Precision.single
-    sig = ob.make_signal(x, "complex", P)
-    p = ob.plan(ns, m, "c2c", 0, n)
-    fs = ob.transform_filters(ob.make_filterset(taps, 0, P), p, "permuted")
-    out = torch.empty((nfil, ns), dtype=torch.complex64, device="cuda")
+    if mode == "r2r":
+        x, taps = x.real, taps.real
+    sig = ob.make_signal(x, "real" if mode == "r2r" else "complex", P)
+    p = ob.plan(ns, m, mode, 0, n)
+    fs = ob.transform_filters(ob.make_filterset(taps, 0, P), p,
+                              "natural" if mode == "r2r" else "permuted")
+    out = torch.empty((nfil, ns), dtype=torch.float32 if mode == "r2r"
+                      else torch.complex64, device="cuda")
     for _ in range(3):
         ob.convolve(sig, fs, p, out=out)
     torch.cuda.synchronize()
@@ -56,7 +61,7 @@ def time_cfg(name, reps=20):
         e1.synchronize()
         ts.append(e0.elapsed_time(e1) * 1e-3)
     t = float(np.median(ts))
-    byts = 8 * ns * (1 + nfil)
+    byts = (4 if mode == "r2r" else 8) * ns * (1 + nfil)
     return t, byts / t / 6546.6e9
 
 
@@ -65,5 +70,6 @@ if __name__ == "__main__":
     err = parity()
     for name in sys.argv[1:]:
         t, frac = time_cfg(name)
-        print(f"variant {v} {name}: {t*1e3:.3f} ms  {frac*100:.1f}% HBM  parity {err:.2e}",
-              flush=True)
+        ns, nfil = CFG[name][0], CFG[name][2]
+        print(f"variant {v} {name}: {t*1e3:.3f} ms  {frac*100:.1f}% HBM  "
+              f"{ns * nfil / t:.3e} outputs/s  parity {err:.2e}", flush=True)
