@@ -37,6 +37,8 @@ extern "C" {
 #define OLSB_PP_NONE 0  /* postproc.py:15  KINDS[0] "none"  */
 #define OLSB_PP_SCALE 1 /* postproc.py:15  KINDS[1] "scale" */
 #define OLSB_PP_MAG2 2  /* postproc.py:15  KINDS[2] "magnitude_squared" */
+#define OLSB_PP_DERIV 3 /* postproc.py:15  KINDS[3] "derivative": central
+                           difference, needs the halo geometry (ols.py:137) */
 
 /* Library version (major * 10000 + minor * 100 + patch). */
 int olsb_version(void);

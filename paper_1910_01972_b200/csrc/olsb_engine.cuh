@@ -864,6 +864,53 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
       // in-place sample p is output o = p - t0 of this segment, kept iff
       // o_lo <= o < o_hi.  With the 32-aligned engine grid every warp store
       // covers one aligned 256-byte chunk of the output row.
+      if constexpr (MODE != FMODE_ABS2) {
+        if (a.pp_kind == OLSB_PP_DERIV) {
+          // non-local epilogue (_store kind 3, _kernels_nb.py:224-262):
+          // central difference of neighbouring samples, one-sided at the
+          // signal ends.  The segment is staged in natural order in this
+          // group's exchange buffer (free after the last exchange) and p +- 1
+          // read back; the halo geometry keeps both inside the segment.
+          const R half = R(0.5);
+          auto dv = [&](long long g, R l, R c, R r) {
+            return g == 0 ? r - c : (g == a.n_s - 1 ? c - l : half * (r - l));
+          };
+          const int pb = G::thread_part(P - 1, t);
+          if constexpr (P == 1) {
+            // one thread holds the whole segment in natural order
+            Cpx<R> d[E];
+            sfor<0, E>([&](auto ec) {
+              constexpr int e = decltype(ec)::value;
+              const Cpx<R> l = y[e > 0 ? e - 1 : 0];
+              const Cpx<R> r = y[e + 1 < E ? e + 1 : E - 1];
+              const long long g = g0 + (e - a.t0);
+              const long long gi = MODE == FMODE_R2R ? g + a.seg_len : g;
+              d[e] = Cpx<R>{dv(g, l.re, y[e].re, r.re),
+                            dv(gi, l.im, y[e].im, r.im)};
+            });
+            sfor<0, E>([&](auto ec) { y[decltype(ec)::value] = d[decltype(ec)::value]; });
+          } else {
+            Cpx<R>* stg = bufs + size_t(sl) * C::L::stride;
+            group_sync<C>(sl);
+            sfor<0, E>([&](auto ec) {
+              constexpr int e = decltype(ec)::value;
+              stg[pb + G::elem_part(P - 1, e)] = y[e];
+            });
+            group_sync<C>(sl);
+            sfor<0, E>([&](auto ec) {
+              constexpr int e = decltype(ec)::value;
+              const int p = pb + G::elem_part(P - 1, e);
+              const Cpx<R> l = stg[p > 0 ? p - 1 : 0];
+              const Cpx<R> r = stg[p + 1 < G::N ? p + 1 : G::N - 1];
+              const long long g = g0 + (p - a.t0);
+              const long long gi = MODE == FMODE_R2R ? g + a.seg_len : g;
+              y[e] = Cpx<R>{dv(g, l.re, y[e].re, r.re),
+                            dv(gi, l.im, y[e].im, r.im)};
+            });
+            if constexpr (C::NBUF == 2) group_sync<C>(sl);  // next exchange
+          }
+        }
+      }
       if constexpr (MODE == FMODE_C2C) {
         const long long goff = (long long)f * a.out_ld + (g0 - a.out_base);
         Cpx<R>* orow = a.out + goff + o0;

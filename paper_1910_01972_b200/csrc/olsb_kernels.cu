@@ -239,7 +239,9 @@ static int fused_range(int mode, const void* x, int64_t x_base, int64_t n_s,
   const int logn = log2_of(n);
   if (logn < 0) return OLSB_E_BAD_LENGTH;
   const bool pp_ok = pp_kind == OLSB_PP_NONE || pp_kind == OLSB_PP_SCALE ||
-                     (mode == FMODE_R2R && pp_kind == OLSB_PP_MAG2);
+                     (mode == FMODE_R2R && pp_kind == OLSB_PP_MAG2) ||
+                     (mode != FMODE_ABS2 && pp_kind == OLSB_PP_DERIV &&
+                      t0 >= 1 && t0 + l_eff <= n - 1);
   if (!pp_ok) return OLSB_E_UNSUPPORTED;
   if (n_s < 1 || n_fil < 0 || g_lo < 0 || g_hi < g_lo) return OLSB_E_BAD_ARG;
   if (l_eff < 1 || t0 < 0 || t0 + l_eff > n) return OLSB_E_GEOMETRY;

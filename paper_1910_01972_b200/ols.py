@@ -294,6 +294,14 @@ def convolve(signal: Signal, filters: FilterSet, seg_plan: SegmentPlan,
     _check_inputs(signal, filters, seg_plan)
     precision = signal.precision
 
+    if pp.kind == "derivative" and (seg_plan.tap_len == 1
+                                    or variant != "fused"):
+        # M = 1 has no halo (the reference recomputes seam neighbours from the
+        # input, _kernels_nb.py:232-260); the comparison variants have no
+        # segment epilogue: plain result, then the global difference on device
+        plain = convolve(signal, filters, seg_plan, variant, None, workers)
+        return _derivative(plain, out)
+
     if variant == "direct_oracle":
         return _direct(signal, filters, pp)
     if variant == "full_fft_baseline":
@@ -326,13 +334,7 @@ def convolve(signal: Signal, filters: FilterSet, seg_plan: SegmentPlan,
                            device=signal.samples.device)
 
     l_eff, t0, win_off, n_seg_eff = _geometry(seg_plan, pp.halo)
-    if pp.kind == "derivative":
-        raise EngineError(
-            "postproc 'derivative' (non-local epilogue) is not in this build's "
-            "engine (SURVEY §8(f) row 3)")
-    if seg_plan.mode == "r2r" and pp.kind not in ("none", "scale",
-                                                  "magnitude_squared"):
-        raise EngineError(f"r2r with postproc {pp.kind!r} is not supported")
+
     if out is not None:
         if tuple(out.shape) != (n_fil, n_s) or out.dtype != out_dtype:
             raise ValueError(f"out must be {(n_fil, n_s)} {out_dtype}")
@@ -342,6 +344,9 @@ def convolve(signal: Signal, filters: FilterSet, seg_plan: SegmentPlan,
     if variant == "fused":
         spec_dev = _engine_spectra(filters)
         if out is not None and not out.is_cuda:
+            if pp.kind == "derivative":
+                raise EngineError("the host streaming path has no 'derivative' "
+                                  "epilogue; convolve into device memory")
             return _fused_streaming(signal, spec_dev, seg_plan, pp, precision,
                                     l_eff, t0, win_off, n_seg_eff, out,
                                     chunk_segments)
@@ -477,6 +482,24 @@ def _fused_streaming(signal, spec_dev, seg_plan, pp, precision, l_eff, t0,
     return out
 
 
+def _derivative(y: torch.Tensor, out: Optional[torch.Tensor] = None):
+    """Global central difference with one-sided ends (postproc.py:44-85 with
+    both ends flagged as signal edges): d[g] = (y[g+1] - y[g-1]) / 2, d[0] =
+    y[1] - y[0], d[-1] = y[-1] - y[-2]."""
+    n_s = y.shape[1]
+    d = torch.empty_like(y)
+    if n_s == 1:
+        d.zero_()
+    else:
+        d[:, 1:n_s - 1] = 0.5 * (y[:, 2:] - y[:, :n_s - 2])
+        d[:, 0] = y[:, 1] - y[:, 0]
+        d[:, n_s - 1] = y[:, n_s - 1] - y[:, n_s - 2]
+    if out is not None:
+        out.copy_(d)
+        return out
+    return d
+
+
 def _pipelined(signal, filters, seg_plan, pp, precision, l_eff, t0, win_off,
                n_seg, out):
     """cuFFT-based OLS, the paper's comparison point (Algorithm 1;
@@ -530,8 +553,6 @@ def _direct(signal: Signal, filters: FilterSet, pp: PostProcSpec):
     """Direct time-domain convolution on the GPU, float64 accumulate, rounded
     to the signal's precision (oracle.py:20-41): y[f,n] = sum_k h[f,k]
     x[n-k+o], zeros off the ends.  Complex conv = 4 real conv1d calls."""
-    if pp.kind == "derivative":
-        raise EngineError("direct_oracle does not support 'derivative'")
     real = signal.value_kind == "real" and filters.value_kind == "real"
     x = signal.samples.to(torch.complex128)
     h = filters.taps.to(torch.complex128)

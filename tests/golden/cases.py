@@ -74,6 +74,16 @@ PP_GRID = [
     (6000, 65, 3, 512, 32, "c2c", "magnitude_squared"),
     (9000, 400, 2, 2048, 0, "c2c", "magnitude_squared"),
     (3000, 9, 2, 16, 8, "c2c", "magnitude_squared"),
+    # derivative: halo geometry (l_eff = L - 2), one-sided at the signal ends
+    (5000, 33, 2, 128, 16, "c2c", "derivative"),
+    (9000, 400, 2, 2048, 0, "c2c", "derivative"),
+    (12000, 1025, 1, 4096, 512, "c2c", "derivative"),
+    (65, 5, 2, 64, 4, "c2c", "derivative"),
+    (2, 3, 1, 8, 1, "c2c", "derivative"),
+    (1000, 1, 2, 64, 0, "c2c", "derivative"),    # M = 1: seam recompute
+    (9000, 400, 3, 2048, 0, "r2r", "derivative"),
+    (5000, 33, 2, 128, 16, "r2r", "derivative"),
+    (1000, 1, 2, 8, 0, "r2r", "derivative"),
 ]
 
 
