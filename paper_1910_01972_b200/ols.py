@@ -636,14 +636,18 @@ def measure_segment_times(tap_len: int, mode: str, candidates: Iterable[int],
     if not feasible:
         raise SegmentTooSmall(
             f"no candidate segment length fits {tap_len} taps")
-    if mode != "c2c":
-        raise EngineError("the fused engine of this build is c2c only")
+    if mode not in MODES:
+        raise ValueError(f"mode must be one of {MODES}, got {mode!r}")
     rng = np.random.default_rng(seed)
-    sig = make_signal(rng.standard_normal(probe_len)
-                      + 1j * rng.standard_normal(probe_len), "complex",
-                      precision)
-    taps = (rng.standard_normal((n_filters, tap_len))
-            + 1j * rng.standard_normal((n_filters, tap_len)))
+    if mode == "r2r":
+        sig = make_signal(rng.standard_normal(probe_len), "real", precision)
+        taps = rng.standard_normal((n_filters, tap_len))
+    else:
+        sig = make_signal(rng.standard_normal(probe_len)
+                          + 1j * rng.standard_normal(probe_len), "complex",
+                          precision)
+        taps = (rng.standard_normal((n_filters, tap_len))
+                + 1j * rng.standard_normal((n_filters, tap_len)))
     fs = make_filterset(taps, 0, precision)
     times = {}
     for cand in feasible:

@@ -120,3 +120,18 @@ def test_fdas_shape_real_full_output_vs_oracle(oc):
     y = oc.convolve(oc.make_signal(x, "real", P), fs, p).cpu().numpy()
     ref = oracle.direct_convolve(x, taps, 0).real
     assert rel_l2_per_filter(y, ref) <= L2_TOL
+
+
+@pytest.mark.parametrize("mode", ["c2c", "r2r"])
+def test_autotune_segment_size(oc, mode):
+    # ols.py:471-526: feasible power-of-two candidates >= max(M, floor),
+    # fastest wins; infeasible candidates are dropped
+    times = oc.measure_segment_times(100, mode, [32, 128, 256, 1024, 3000],
+                                     probe_len=1 << 16, n_filters=2)
+    assert sorted(times) == [128, 256, 1024]
+    assert all(t > 0 for t in times.values())
+    best = oc.autotune_segment_size(100, mode, [128, 256, 1024],
+                                    probe_len=1 << 16, n_filters=2)
+    assert best in (128, 256, 1024)
+    with pytest.raises(oc.SegmentTooSmall):
+        oc.measure_segment_times(100, mode, [16, 64])
