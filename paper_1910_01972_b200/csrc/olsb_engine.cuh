@@ -54,7 +54,8 @@ enum HMode : int {
 // barrier scope (0: CTA-wide __syncthreads, 1: named barrier per group),
 // MINB target CTAs per SM (register cap).
 template <class R_, int LOGN_, int SEGS_, int NBUF_, int HM_, int BAR_,
-          int MINB_, int MIDREG_ = 0, int TMX_ = 0, int PREF_ = 0>
+          int MINB_, int MIDREG_ = 0, int TMX_ = 0, int PREF_ = 0,
+          int ABL_ = 0>
 struct KCfg {
   using R = R_;
   static constexpr int LOGN = LOGN_;
@@ -91,6 +92,11 @@ struct KCfg {
   // H_TEX only: the next filter's spectrum is fetched into registers while
   // the current one is transformed (hides the L2 latency of the fetch)
   static constexpr bool PREF = PREF_ && HM_ == H_TEX && !dbl;
+  // ablation switches for bottleneck analysis (results are wrong with any
+  // bit set): 1 no output stores, 2 no shared-memory traffic in the inverse
+  // exchanges, 4 no inverse exchange barriers, 8 spectra of filters f & 1
+  // only (L1-resident: isolates the L2 traffic of the spectrum fetches)
+  static constexpr int ABL = ABL_;
   static constexpr bool TOPREG = !dbl && P >= 2 && !TMX;
   // the top window's table is built in the exchange buffers (TOPREG / TMX)
   static constexpr bool TOPOUT = TOPREG || TMX;
@@ -444,20 +450,22 @@ struct NoHook {
 
 // exchange: write window QW, barrier, read window QR.  `pre_bar` runs after
 // the stores, right before the barrier (used to fold a producer wait into it)
-template <class C, int QW, int QR, class H = NoHook, class H2 = NoHook>
+template <class C, int QW, int QR, class H = NoHook, class H2 = NoHook,
+          int ABL = 0>
 __device__ __forceinline__ void exchange(Cpx<typename C::R>* bufs, int& xc,
                                          int sl, int t, Cpx<typename C::R>* x,
                                          const H& pre_bar = H{},
-                                         const H2& post_bar = H2{}) {
+                                         const H2& post_bar = H2{},
+                                         IC<ABL> = {}) {
   Cpx<typename C::R>* buf = bufs + (C::NBUF == 2 ? (xc & 1) * C::buf_elems : 0) +
                             size_t(sl) * C::L::stride;
   constexpr int X = QW < QR ? QW : QR;  // exchange between windows X, X+1
-  if constexpr (C::NBUF == 1) group_sync<C>(sl);
-  smem_store<C, QW, X>(buf, t, x);
+  if constexpr (C::NBUF == 1 && !(ABL & 4)) group_sync<C>(sl);
+  if constexpr (!(ABL & 2)) smem_store<C, QW, X>(buf, t, x);
   pre_bar();
-  group_sync<C>(sl);
+  if constexpr (!(ABL & 4)) group_sync<C>(sl);
   post_bar();
-  smem_load<C, QR, X>(buf, t, x);
+  if constexpr (!(ABL & 2)) smem_load<C, QR, X>(buf, t, x);
   ++xc;
 }
 
@@ -663,7 +671,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   float4 hn[C::PREF ? C::VPT : 1];
   auto fetch = [&](int f) {
     if constexpr (C::PREF) {
-      const int hb = f * (C::VPT * T) + t;
+      const int hb = ((C::ABL & 8) ? (f & 1) : f) * (C::VPT * T) + t;
       sfor<0, C::VPT>([&](auto uc) {
         constexpr int u = decltype(uc)::value;
         hn[u] = tex1Dfetch<float4>(a.htex, hb + u * T);
@@ -695,7 +703,9 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     auto seg_mask = [&](long long g, long long& olo, unsigned& sp) {
       olo = a.g_lo > g ? a.g_lo - g : 0;
       const long long ohi = a.g_hi - g < a.seg_len ? a.g_hi - g : a.seg_len;
-      sp = (!live || (a.dbg & 1) || ohi <= olo) ? 0u : unsigned(ohi - olo);
+      sp = (!live || (a.dbg & 1) || (C::ABL & 1) || ohi <= olo)
+               ? 0u
+               : unsigned(ohi - olo);
       unsigned m = 0;
       sfor<0, E>([&](auto ec) {
         constexpr int e = decltype(ec)::value;
@@ -842,9 +852,11 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
       sfor<1, P>([&](auto qc) {
         constexpr int q = decltype(qc)::value;
         if constexpr (q == P - 1) {
-          exchange<C, q - 1, q>(bufs, xc, sl, t, y, wait_next);
+          exchange<C, q - 1, q>(bufs, xc, sl, t, y, wait_next, NoHook{},
+                                IC<C::ABL>{});
         } else {
-          exchange<C, q - 1, q>(bufs, xc, sl, t, y);
+          exchange<C, q - 1, q>(bufs, xc, sl, t, y, NoHook{}, NoHook{},
+                                IC<C::ABL>{});
         }
         if constexpr (C::TMX && (q == P - 1 || (q == P - 2 && C::TMX == 2))) {
           Tw<R> tw[16];

@@ -66,14 +66,16 @@ struct DefaultPolicy {
 template <int LOGN, int V>
 struct Variant {
   static constexpr int T = Geo<LOGN>::T;
-  // {SEGS, NBUF, HM, BAR, MINB (warpgroups/SM), MIDREG, TMX, PREF}
-  static constexpr int tab[4][8] = {
-      {1, 1, H_TEX, 0, 4, 0, 0, 0}, {1, 1, H_TEX, 0, 4, 0, 1, 1},
-      {1, 1, H_TEX, 0, 4, 0, 2, 1}, {1, 2, H_TEX, 0, 4, 0, 2, 1}};
+  // {SEGS, NBUF, HM, BAR, MINB (warpgroups/SM), MIDREG, TMX, PREF, ABL}
+  static constexpr int tab[8][9] = {
+      {1, 1, H_TEX, 0, 4, 0, 0, 0, 0}, {1, 1, H_TEX, 0, 4, 0, 1, 1, 0},
+      {1, 1, H_TEX, 0, 4, 0, 2, 1, 0}, {1, 2, H_TEX, 0, 4, 0, 2, 1, 0},
+      {1, 1, H_TEX, 0, 4, 0, 2, 1, 1}, {1, 1, H_TEX, 0, 4, 0, 2, 1, 6},
+      {1, 1, H_TEX, 0, 4, 0, 2, 1, 8}, {1, 1, H_TEX, 0, 4, 0, 2, 1, 14}};
   static constexpr int segs = tab[V][0] * std::max(1, 128 / T);
   static constexpr int minb = std::max(1, tab[V][4] * 128 / (segs * T));
   using type = KCfg<float, LOGN, segs, tab[V][1], tab[V][2], tab[V][3], minb,
-                    tab[V][5], tab[V][6], tab[V][7]>;
+                    tab[V][5], tab[V][6], tab[V][7], tab[V][8]>;
 };
 
 inline int debug_env() {
@@ -127,6 +129,10 @@ int launch_fused(FusedArgs<R> a, int mode, cudaStream_t st) {
       case 1: return launch_fused_cfg<typename Variant<LOGN, 1>::type>(a, st);
       case 2: return launch_fused_cfg<typename Variant<LOGN, 2>::type>(a, st);
       case 3: return launch_fused_cfg<typename Variant<LOGN, 3>::type>(a, st);
+      case 4: return launch_fused_cfg<typename Variant<LOGN, 4>::type>(a, st);
+      case 5: return launch_fused_cfg<typename Variant<LOGN, 5>::type>(a, st);
+      case 6: return launch_fused_cfg<typename Variant<LOGN, 6>::type>(a, st);
+      case 7: return launch_fused_cfg<typename Variant<LOGN, 7>::type>(a, st);
       default: break;
     }
   }
