@@ -120,7 +120,8 @@ def convolve_shard(x_local: torch.Tensor, shard: Shard, seg_plan: SegmentPlan,
     from .postproc import NONE
     pp = postproc or NONE
     if filters.spectra is None:
-        filters = transform_filters(filters, seg_plan, "permuted")
+        filters = transform_filters(
+            filters, seg_plan, "natural" if seg_plan.mode == "r2r" else "permuted")
     spec = _engine_spectra(filters)
     width = shard.g_hi - shard.g_lo
     if out is None:

@@ -31,9 +31,10 @@ CASES = [
 ]
 
 
-def test_shards_partition_and_cover_dependencies():
+@pytest.mark.parametrize("mode", ["c2c", "r2r"])
+def test_shards_partition_and_cover_dependencies(mode):
     for ns, m, nfil, n, origin in CASES:
-        p = oc.plan(ns, m, "c2c", origin, n)
+        p = oc.plan(ns, m, mode, origin, n)
         for world in (1, 2, 3, 8, 64):
             sh = make_shards(p, world)
             assert len(sh) == world
