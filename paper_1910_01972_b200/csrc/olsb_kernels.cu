@@ -33,6 +33,35 @@ namespace olsb {
 
 int g_filter_chunk = 0;
 
+// (kernel, device) -> resident CTAs, for prepare() (olsb_launch.cuh)
+struct Prepared {
+  const void* kernel;
+  int dev, resident;
+};
+static std::mutex g_prep_mu;
+static Prepared g_prep[512];
+static int g_prep_n = 0;
+
+int prepared_lookup(const void* kernel, int* resident) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_prep_mu);
+  for (int i = 0; i < g_prep_n; ++i) {
+    if (g_prep[i].kernel == kernel && g_prep[i].dev == dev) {
+      *resident = g_prep[i].resident;
+      return 1;
+    }
+  }
+  return 0;
+}
+
+void prepared_store(const void* kernel, int resident) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_prep_mu);
+  if (g_prep_n < 512) g_prep[g_prep_n++] = Prepared{kernel, dev, resident};
+}
+
 // Texture objects over engine-layout spectra (H_TEX), cached per
 // (device, pointer, size); creating one costs microseconds, so a FilterSet
 // reused across calls pays it once.

@@ -26,8 +26,15 @@ inline int num_sms() {
   return n > 0 ? n : 1;
 }
 
+// Kernel attributes + resident CTA count, done once per (kernel, device):
+// the attribute call and the occupancy query cost microseconds, which is the
+// whole budget of a small convolution (cache in olsb_kernels.cu).
+int prepared_lookup(const void* kernel, int* resident);
+void prepared_store(const void* kernel, int resident);
+
 template <class K>
 int prepare(K kernel, size_t smem, int threads, int* resident) {
+  if (prepared_lookup(reinterpret_cast<const void*>(kernel), resident)) return 0;
   cudaError_t e = cudaFuncSetAttribute(
       kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return int(e);
@@ -36,6 +43,7 @@ int prepare(K kernel, size_t smem, int threads, int* resident) {
                                                     smem);
   if (e != cudaSuccess) return int(e);
   *resident = std::max(1, occ) * num_sms();
+  prepared_store(reinterpret_cast<const void*>(kernel), *resident);
   return 0;
 }
 
