@@ -189,15 +189,9 @@ def transform_filters(filters: FilterSet, seg_plan: SegmentPlan,
         spectra = torch.fft.rfft(padded, dim=1)
         # the fused real engine transforms two real segments as one complex
         # one, so it multiplies by the full complex spectrum of the real taps
-        # (engine layout, same in-register FFT as the c2c path)
-        ctaps = taps.to(precision.torch_complex).contiguous()
-        dev = torch.empty((filters.n_filters, n), dtype=precision.torch_complex,
-                          device=taps.device)
-        with torch.cuda.device(taps.device):
-            _lib.call("olsb_filter_spectra_c2c", ctaps.data_ptr(),
-                      filters.n_filters, filters.tap_length, n, None,
-                      dev.data_ptr(), precision.code, _stream_ptr())
-        return filters.with_spectra(spectra, layout, n, dev)
+        # (engine layout, same in-register FFT as the c2c path); built on
+        # first use by _engine_spectra (segment lengths the engine supports)
+        return filters.with_spectra(spectra, layout, n)
     ctaps = taps.to(precision.torch_complex).contiguous()
     if layout == "permuted":
         spectra = torch.empty((filters.n_filters, n),
@@ -229,9 +223,10 @@ def _engine_spectra(filters: FilterSet) -> torch.Tensor:
         ctaps = filters.taps.to(prec.torch_complex).contiguous()
         dev = torch.empty((filters.n_filters, n), dtype=prec.torch_complex,
                           device=ctaps.device)
-        _lib.call("olsb_filter_spectra_c2c", ctaps.data_ptr(),
-                  filters.n_filters, filters.tap_length, n, None,
-                  dev.data_ptr(), prec.code, _stream_ptr())
+        with torch.cuda.device(ctaps.device):
+            _lib.call("olsb_filter_spectra_c2c", ctaps.data_ptr(),
+                      filters.n_filters, filters.tap_length, n, None,
+                      dev.data_ptr(), prec.code, _stream_ptr())
         object.__setattr__(filters, "spectra_dev", dev)
         return dev
     spec = filters.spectra.contiguous()

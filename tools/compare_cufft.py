@@ -4,9 +4,9 @@ at FFT lengths <= 4096).
     python tools/compare_cufft.py [cfg ...]
 
 For every config: the fused engine at the config's N, and the cuFFT OLS
-(`convolve(variant="pipelined")`: gather -> batched C2C cuFFT -> multiply ->
-batched inverse C2C -> discard, chunked over segments, the paper's Algorithm
-1) at the same N and at its own best N in {N, 8192, 16384}.  CUDA events,
+(`convolve(variant="pipelined")`: gather -> batched C2C (real path: R2C)
+cuFFT -> multiply -> batched inverse C2C (C2R) -> discard, chunked over
+segments, the paper's Algorithm 1) at the same N and at its own best N in {N, 8192, 16384}.  CUDA events,
 median of 5 after 2 warm-ups, inputs resident, outputs preallocated.
 Prints one JSON line per config.
 """
@@ -44,24 +44,30 @@ def timed(fn, reps=5, warm=2):
 
 
 def run(name):
-    ns, m, nfil, n = CFG[name]
+    ns, m, nfil, n, *mode = CFG[name]
+    mode = mode[0] if mode else "c2c"
     x, taps = gen_inputs(ns, m, nfil)
+    if mode == "r2r":
+        x, taps = x.real, taps.real
     P = ob.Precision.single
-    sig = ob.make_signal(x, "complex", P)
+    sig = ob.make_signal(x, "real" if mode == "r2r" else "complex", P)
     fset = ob.make_filterset(taps, 0, P)
-    out = torch.empty((nfil, ns), dtype=torch.complex64, device="cuda")
-    p = ob.plan(ns, m, "c2c", 0, n)
-    fs = ob.transform_filters(fset, p, "permuted")
+    out = torch.empty((nfil, ns), dtype=torch.float32 if mode == "r2r"
+                      else torch.complex64, device="cuda")
+    p = ob.plan(ns, m, mode, 0, n)
+    fs = ob.transform_filters(fset, p,
+                              "natural" if mode == "r2r" else "permuted")
     t_fused = timed(lambda: ob.convolve(sig, fs, p, out=out))
     ref = out.clone()
-    res = {"cfg": name, "n_s": ns, "m": m, "filters": nfil, "fft_len": n,
+    res = {"cfg": name, "mode": mode, "n_s": ns, "m": m, "filters": nfil,
+           "fft_len": n,
            "fused_ms": t_fused * 1e3,
            "fused_outputs_per_s": ns * nfil / t_fused}
     best = None
     for nc in sorted({n, 8192, 16384}):
         if nc < m:
             continue
-        pc = ob.plan(ns, m, "c2c", 0, nc, max_fft_len=max(nc, 4096))
+        pc = ob.plan(ns, m, mode, 0, nc, max_fft_len=max(nc, 4096))
         fc = ob.transform_filters(fset, pc, "natural")
         t = timed(lambda: ob.convolve(sig, fc, pc, variant="pipelined",
                                       out=out), reps=3, warm=1)
@@ -80,6 +86,7 @@ def run(name):
 if __name__ == "__main__":
     names = sys.argv[1:] or ["cfg1", "cfg2_n256", "cfg2_n512", "cfg2_n1024",
                              "cfg2_n2048", "cfg2_n4096", "cfg3", "cfg4_m8_f8",
-                             "cfg4_m32_f8"]
+                             "cfg4_m32_f8", "cfg3_r2r", "cfg2_n1024_r2r",
+                             "cfg2_n4096_r2r"]
     for nm in names:
         print(json.dumps(run(nm)), flush=True)
