@@ -16,7 +16,8 @@ from .errors import EngineError
 
 _LOCK = threading.Lock()
 _LIB = None
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libolsb.so")
+LIB_PATH = os.environ.get("OLSB_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "libolsb.so")
 
 c_int, c_i64, c_vp, c_dbl = ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, ctypes.c_double
 

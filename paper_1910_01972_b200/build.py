@@ -64,7 +64,8 @@ def build(verbose: bool = False, force: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     os.makedirs(OBJDIR, exist_ok=True)
-    base = [nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC]
+    base = [nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC,
+            *os.environ.get("OLSB_NVCC_EXTRA", "").split()]
     if verbose:
         base += ["-Xptxas", "-v"]
     jobs = [(base + ["-c", SOURCES[0], "-o",

@@ -141,7 +141,11 @@ using RowCfg = KCfg<R, LOGN,
 // ---------------------------------------------------------------------------
 template <class C>
 __device__ __forceinline__ void group_sync(int sl) {
-  if constexpr (C::BAR == 1) {
+  if constexpr (C::T <= 32) {
+    // a segment group lives inside one warp (N <= 512): warp-level sync
+    // orders its shared-memory exchange; other warps are independent
+    __syncwarp();
+  } else if constexpr (C::BAR == 1) {
     asm volatile("bar.sync %0, %1;" ::"r"(1 + sl), "r"(C::T) : "memory");
   } else {
     __syncthreads();
@@ -460,10 +464,22 @@ __device__ __forceinline__ void exchange(Cpx<typename C::R>* bufs, int& xc,
   Cpx<typename C::R>* buf = bufs + (C::NBUF == 2 ? (xc & 1) * C::buf_elems : 0) +
                             size_t(sl) * C::L::stride;
   constexpr int X = QW < QR ? QW : QR;  // exchange between windows X, X+1
+  // warp-local exchange (Geo::warp_local): a warp reads back only what it
+  // wrote, so the store -> load sync is warp-level.  The sync BEFORE the
+  // stores stays group-wide: the buffer's previous user may be a cross-warp
+  // exchange whose loads other warps are still issuing.  (Not with TMA
+  // spectra: their barrier also publishes the mbarrier wait.)
+  constexpr bool WL = C::G::warp_local(X) && C::HM != H_TMA;
   if constexpr (C::NBUF == 1 && !(ABL & 4)) group_sync<C>(sl);
   if constexpr (!(ABL & 2)) smem_store<C, QW, X>(buf, t, x);
   pre_bar();
-  if constexpr (!(ABL & 4)) group_sync<C>(sl);
+  if constexpr (!(ABL & 4)) {
+    if constexpr (WL) {
+      __syncwarp();
+    } else {
+      group_sync<C>(sl);
+    }
+  }
   post_bar();
   if constexpr (!(ABL & 2)) smem_load<C, QR, X>(buf, t, x);
   ++xc;

@@ -66,6 +66,10 @@ OLSB_HD void sfor(F&& f) {
 // N = 2^LOGN.  E = min(16, N) samples per thread, T = N / E threads per
 // segment, P windows.  Window 0 ("J", the junction) holds index bits
 // [0, G0) (plus G0..3 as batch bits); window q >= 1 holds bits [lo, lo+4).
+#ifndef OLSB_MID_REMAP
+#define OLSB_MID_REMAP 1
+#endif
+
 template <int LOGN_>
 struct Geo {
   static constexpr int LOGN = LOGN_;
@@ -88,13 +92,14 @@ struct Geo {
   // holds iff lo >= 7; a lower window with at least two warp bits to spare
   // swaps thread bits (lo-2, lo-1) with the top two thread bits instead.
   static constexpr bool remap(int q) {
-    return q >= 1 && lo(q) >= 2 && lo(q) < 7 && LOGT >= 7 && lo(q) <= LOGT - 2;
+    return OLSB_MID_REMAP && q >= 1 && lo(q) >= 2 && lo(q) < 7 && LOGT >= 7 &&
+           lo(q) <= LOGT - 2;
   }
   // windows whose first two stages use the FMA (tangent) forms
   static constexpr bool tan01(int q) {
     return q >= 1 && (lo(q) >= 7 || remap(q));
   }
-  static OLSB_HD int perm(int q, int t) {
+  static OLSB_HD constexpr int perm(int q, int t) {
     if (!remap(q)) return t;
     const int a = remap(q) ? lo(q) - 2 : 0, b = remap(q) ? LOGT - 2 : 0;
     const int x = ((t >> a) ^ (t >> b)) & 3;  // swap two 2-bit fields
@@ -108,7 +113,7 @@ struct Geo {
   static constexpr int tw_total() { return tw_offset(P); }
   // thread part / element part of the in-place index in window q (disjoint
   // bit fields, so p = thread_part + elem_part)
-  static OLSB_HD int thread_part(int q, int t) {
+  static OLSB_HD constexpr int thread_part(int q, int t) {
     const int l = lo(q);
     const int u = perm(q, t);
     return ((u >> l) << (l + LOGE)) | (u & ((1 << l) - 1));
@@ -116,6 +121,14 @@ struct Geo {
   static constexpr int elem_part(int q, int e) { return e << lo(q); }
   static OLSB_HD int low_bits(int q, int t) {
     return perm(q, t) & ((1 << lo(q)) - 1);
+  }
+  // Exchange x (windows x <-> x+1) is warp-local when every warp bit (thread
+  // bits 5 .. LOGT-1) maps to the same index bit in both windows: each warp
+  // then reads back only what it wrote, and a warp-level sync suffices.
+  static constexpr bool warp_local(int x) {
+    for (int b = 5; b < LOGT; ++b)
+      if (thread_part(x, 1 << b) != thread_part(x + 1, 1 << b)) return false;
+    return true;
   }
 };
 
