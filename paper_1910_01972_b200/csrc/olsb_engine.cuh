@@ -40,13 +40,11 @@ struct V16<double> {
   static constexpr int per = 1;
 };
 
-// How the fused kernel stages filter spectra:
+// How the fused kernel fetches filter spectra:
 enum HMode : int {
-  H_LDG = 0,    // read through L1 with __ldg at the multiply
-  H_TMA = 1,    // CTA-shared double buffer filled by TMA bulk copies
-  H_ASYNC = 2,  // per-thread cp.async prefetch of the next filter's values
-  H_TEX = 3,    // texture fetches: the TEX data path runs beside the LSU
-                // pipe that carries the shared-memory exchanges
+  H_LDG = 0,  // read through L1 with __ldg at the multiply (fp64 policy)
+  H_TEX = 3,  // texture fetches: the TEX data path runs beside the LSU pipe
+              // that carries the shared-memory exchanges (fp32 policies)
 };
 
 // Kernel configuration.  SEGS segment groups per CTA, NBUF exchange buffers
@@ -54,8 +52,7 @@ enum HMode : int {
 // barrier scope (0: CTA-wide __syncthreads, 1: named barrier per group),
 // MINB target CTAs per SM (register cap).
 template <class R_, int LOGN_, int SEGS_, int NBUF_, int HM_, int BAR_,
-          int MINB_, int MIDREG_ = 0, int TMX_ = 0, int PREF_ = 0,
-          int ABL_ = 0>
+          int MINB_, int TMX_ = 0, int PREF_ = 0, int ABL_ = 0>
 struct KCfg {
   using R = R_;
   static constexpr int LOGN = LOGN_;
@@ -100,9 +97,6 @@ struct KCfg {
   static constexpr bool TOPREG = !dbl && P >= 2 && !TMX;
   // the top window's table is built in the exchange buffers (TOPREG / TMX)
   static constexpr bool TOPOUT = TOPREG || TMX;
-  // the window below the top one keeps its twiddles in registers as well
-  // (fused kernel only): no shared-memory twiddle reads in the filter loop
-  static constexpr bool MIDREG = TOPREG && MIDREG_ && P >= 3;
   static constexpr size_t al(size_t b) { return (b + 127) & ~size_t(127); }
   static constexpr size_t buf_elems = size_t(SEGS) * L::stride;
   static constexpr size_t bufs_bytes =
@@ -110,7 +104,7 @@ struct KCfg {
   // ---- row kernels: every twiddle table in shared memory, then buffers
   static constexpr size_t tab_bytes = al(size_t(G::tw_total()) * sizeof(Tw<R>));
   static constexpr size_t smem_bytes = tab_bytes + bufs_bytes;
-  // ---- fused kernel: [bufs (+ top table at init) | low tables | H | bars]
+  // ---- fused kernel: [bufs (+ top table at init) | low tables | TMEM slot]
   static constexpr int lowtab_elems = TOPOUT ? G::tw_offset(P - 1) : G::tw_total();
   static constexpr size_t f_bufs_bytes =
       P >= 2 ? std::max(bufs_bytes,
@@ -119,14 +113,9 @@ struct KCfg {
              : 0;
   static constexpr size_t f_tab_off = f_bufs_bytes;
   static constexpr size_t f_tab_bytes = al(size_t(lowtab_elems) * sizeof(Tw<R>));
-  static constexpr size_t f_h_off = f_tab_off + f_tab_bytes;
-  static constexpr size_t h_bytes = size_t(G::N) * sizeof(Cpx<R>);
-  static constexpr size_t f_h_bytes =
-      HM == H_TMA ? 2 * h_bytes
-                  : (HM == H_ASYNC ? al(size_t(THREADS) * VPT * 16) : 0);
-  static constexpr size_t f_bar_off = f_h_off + f_h_bytes;
-  // [2 mbarriers | TMEM base address slot]
-  static constexpr size_t f_smem_bytes = f_bar_off + 32;
+  static constexpr size_t f_slot_off = f_tab_off + f_tab_bytes;
+  // [TMEM base address slot]
+  static constexpr size_t f_smem_bytes = f_slot_off + 16;
 };
 
 // configuration of the row kernels (filter spectra, standalone transforms)
@@ -232,53 +221,10 @@ __device__ void build_tables(Tw<R>* lowtab, Tw<R>* toptab) {
   });
 }
 
-// ---- TMA bulk copy + mbarrier, cp.async
+// ---- shared-memory address for PTX operands
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(count)
-               : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-// one elected thread: global -> shared bulk copy completing on `bar`
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src,
-                                        uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-          smem_u32(bar)),
-      "r"(bytes)
-      : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
-      "[%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "OLSB_WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra OLSB_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)),
-               "l"(src)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-}
-
 // ---- tensor memory (tcgen05) as per-thread storage.  Thread i of warp w
 // owns TMEM lane 32 (w % 4) + i; `ta` = allocation base + lane + column.
 template <int COLS>
@@ -448,18 +394,11 @@ __device__ __forceinline__ int top_bits(int t) {
   return G::lo(Q) >= 2 ? (G::low_bits(Q, t) >> (G::lo(Q) - 2)) & 3 : 0;
 }
 
-struct NoHook {
-  __device__ __forceinline__ void operator()() const {}
-};
 
-// exchange: write window QW, barrier, read window QR.  `pre_bar` runs after
-// the stores, right before the barrier (used to fold a producer wait into it)
-template <class C, int QW, int QR, class H = NoHook, class H2 = NoHook,
-          int ABL = 0>
+// exchange: write window QW, barrier, read window QR (ABL: ablation bits)
+template <class C, int QW, int QR, int ABL = 0>
 __device__ __forceinline__ void exchange(Cpx<typename C::R>* bufs, int& xc,
                                          int sl, int t, Cpx<typename C::R>* x,
-                                         const H& pre_bar = H{},
-                                         const H2& post_bar = H2{},
                                          IC<ABL> = {}) {
   Cpx<typename C::R>* buf = bufs + (C::NBUF == 2 ? (xc & 1) * C::buf_elems : 0) +
                             size_t(sl) * C::L::stride;
@@ -467,12 +406,10 @@ __device__ __forceinline__ void exchange(Cpx<typename C::R>* bufs, int& xc,
   // warp-local exchange (Geo::warp_local): a warp reads back only what it
   // wrote, so the store -> load sync is warp-level.  The sync BEFORE the
   // stores stays group-wide: the buffer's previous user may be a cross-warp
-  // exchange whose loads other warps are still issuing.  (Not with TMA
-  // spectra: their barrier also publishes the mbarrier wait.)
-  constexpr bool WL = C::G::warp_local(X) && C::HM != H_TMA;
+  // exchange whose loads other warps are still issuing.
+  constexpr bool WL = C::G::warp_local(X);
   if constexpr (C::NBUF == 1 && !(ABL & 4)) group_sync<C>(sl);
   if constexpr (!(ABL & 2)) smem_store<C, QW, X>(buf, t, x);
-  pre_bar();
   if constexpr (!(ABL & 4)) {
     if constexpr (WL) {
       __syncwarp();
@@ -480,35 +417,25 @@ __device__ __forceinline__ void exchange(Cpx<typename C::R>* bufs, int& xc,
       group_sync<C>(sl);
     }
   }
-  post_bar();
   if constexpr (!(ABL & 2)) smem_load<C, QR, X>(buf, t, x);
   ++xc;
 }
 
 // full forward transform: x holds window P-1 on entry, window 0 (J) on exit.
-// With TOPREG the top window's 15 twiddles come from `twr`, with MIDREG the
-// next window's from `twm`; with TMX they are read from TMEM at `tb`.
-template <class C, bool TOPREG, bool MIDREG = false, class H = NoHook,
-          class H2 = NoHook>
+// With TOPREG the top window's 15 twiddles come from `twr`; with TMX the
+// runtime windows' twiddles are read from TMEM at `tb`.
+template <class C, bool TOPREG>
 __device__ __forceinline__ void forward_fft(Cpx<typename C::R>* x,
                                             const Tw<typename C::R>* lowtab,
                                             const Tw<typename C::R>* twr,
-                                            const Tw<typename C::R>* twm,
                                             Cpx<typename C::R>* bufs, int& xc,
-                                            int sl, int t,
-                                            const H& last_hook = H{},
-                                            const H2& post_hook = H2{},
-                                            uint32_t tb = 0) {
+                                            int sl, int t, uint32_t tb = 0) {
   using R = typename C::R;
   using G = typename C::G;
   constexpr int LOGN = C::LOGN;
   sfor<0, G::P>([&](auto qr) {
     constexpr int q = G::P - 1 - decltype(qr)::value;
-    if constexpr (q == 0 && G::P > 1) {
-      exchange<C, q + 1, q>(bufs, xc, sl, t, x, last_hook, post_hook);
-    } else if constexpr (q < G::P - 1) {
-      exchange<C, q + 1, q>(bufs, xc, sl, t, x, NoHook{}, post_hook);
-    }
+    if constexpr (q < G::P - 1) exchange<C, q + 1, q>(bufs, xc, sl, t, x);
     if constexpr (q == 0) {
       dif_pass_static<R, C::LOGE, G::G0>(x);
     } else {
@@ -518,8 +445,6 @@ __device__ __forceinline__ void forward_fft(Cpx<typename C::R>* x,
         dif_pass_rt<R, G::tan01(q)>(x, TwRegs<R>{tw}, top_bits<LOGN, q>(t));
       } else if constexpr (q == G::P - 1 && TOPREG) {
         dif_pass_rt<R, G::tan01(q)>(x, TwRegs<R>{twr}, top_bits<LOGN, q>(t));
-      } else if constexpr (q == G::P - 2 && MIDREG) {
-        dif_pass_rt<R, G::tan01(q)>(x, TwRegs<R>{twm}, top_bits<LOGN, q>(t));
       } else {
         dif_pass_rt<R, G::tan01(q)>(
             x, tw_smem<R, LOGN, q>(lowtab + G::tw_offset(q), t),
@@ -593,9 +518,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Cpx<R>* bufs = reinterpret_cast<Cpx<R>*>(smem_raw);
   Tw<R>* lowtab = reinterpret_cast<Tw<R>*>(smem_raw + C::f_tab_off);
-  Cpx<R>* hbuf = reinterpret_cast<Cpx<R>*>(smem_raw + C::f_h_off);
-  uint64_t* hbar = reinterpret_cast<uint64_t*>(smem_raw + C::f_bar_off);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem_raw + C::f_bar_off + 16);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem_raw + C::f_slot_off);
 
   const int tid = threadIdx.x;
   const int sl = tid / T;
@@ -607,13 +530,6 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   const int nfch = (a.n_fil + a.fchunk - 1) / a.fchunk;
   const long long nitems = ngroups * nfch;
 
-  if constexpr (C::HM == H_TMA) {
-    if (tid == 0) {
-      mbar_init(&hbar[0], 1);
-      mbar_init(&hbar[1], 1);
-      fence_proxy_async();
-    }
-  }
   if constexpr (C::TMX) {
     if (tid < 32) tmem_alloc<C::TCOLS>(tslot);
     tmem_fence_before();
@@ -629,10 +545,11 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     tb = tbase + (uint32_t((w & 3) * 32) << 16) + uint32_t((w >> 2) * C::CPW);
   }
 
-  // top-window twiddles: fixed per thread for the kernel lifetime
+  // runtime-window twiddles: fixed per thread for the kernel lifetime, in
+  // registers (TOPREG) or TMEM (TMX)
   Tw<R> twr[15];
-  Tw<R> twm[15];
-  if constexpr (C::MIDREG || C::TMX == 2) {
+  if constexpr (C::TMX == 2) {
+    Tw<R> twm[15];
     constexpr int q = P - 2;
     const TwSmem<R> tt = tw_smem<R, LOGN, q>(lowtab + G::tw_offset(q), t);
     twm[0] = tt.get0();
@@ -642,7 +559,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
       twm[2 * pp - 1] = w.a;
       twm[2 * pp] = w.b;
     }
-    if constexpr (C::TMX == 2) tmem_st_tw(tb + 64, twm);
+    tmem_st_tw(tb + 64, twm);
   }
   if constexpr (C::TOPOUT) {
     constexpr int q = P - 1;
@@ -662,28 +579,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     __syncthreads();  // the exchange buffers are free from here on
   }
 
-  // ---- filter-spectrum staging
-  // H_TMA: the (item, filter) pairs this CTA visits, in order; pair i lands
-  // in hbuf[i & 1] (TMA bulk copy issued one pair ahead by thread 0)
-  auto issue = [&](int f, int slot) {
-    if constexpr (C::HM == H_TMA) {
-      bulk_g2s(hbuf + size_t(slot) * G::N, a.spec + size_t(f) * C::VPT * T,
-               uint32_t(C::h_bytes), &hbar[slot]);
-    }
-  };
-  // H_ASYNC: this thread's VPT vectors of filter f -> its private slots
-  float4* hpriv = reinterpret_cast<float4*>(hbuf) + tid;
-  auto prefetch = [&](int f) {
-    if constexpr (C::HM == H_ASYNC) {
-      const float4* src = reinterpret_cast<const float4*>(a.spec) +
-                          size_t(f) * C::VPT * T + t;
-#pragma unroll
-      for (int u = 0; u < C::VPT; ++u)
-        cp_async16(hpriv + u * C::THREADS, src + u * T);
-      cp_async_commit();
-    }
-  };
-  // PREF: this thread's VPT vectors of the next filter, in registers
+  // ---- filter-spectrum staging.  PREF: this thread's VPT vectors of the next filter, in registers
   float4 hn[C::PREF ? C::VPT : 1];
   auto fetch = [&](int f) {
     if constexpr (C::PREF) {
@@ -696,14 +592,11 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   };
   if (blockIdx.x < nitems) {
     const int f0 = int(blockIdx.x % nfch) * a.fchunk;
-    if (C::HM == H_TMA && tid == 0) issue(f0, 0);
-    prefetch(f0);
     fetch(f0);
   }
 
   const R inv_n = R(1) / R(G::N);
   int xc = 0;
-  unsigned hseq = 0;
 
   for (long long it = blockIdx.x; it < nitems; it += gridDim.x) {
     const long long grp = it / nfch;
@@ -780,16 +673,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     }
     // ---- forward FFT (dif_fwd, _kernels_nb.py:11-28); the spectrum stays in
     // registers (or TMEM) with the inverse's 1/N and the scale post-process
-    // folded in.  H_TMA: thread 0 makes sure this item's first spectrum has
-    // landed before the forward FFT's last barrier; everybody else learns it
-    // from the barrier
-    auto wait_cur = [&]() {
-      if constexpr (C::HM == H_TMA && P > 1) {
-        if (tid == 0) mbar_wait(&hbar[hseq & 1u], (hseq >> 1) & 1u);
-      }
-    };
-    forward_fft<C, C::TOPREG, C::MIDREG>(x, lowtab, twr, twm, bufs, xc, sl, t,
-                                         wait_cur, NoHook{}, tb);
+    // folded in
+    forward_fft<C, C::TOPREG>(x, lowtab, twr, bufs, xc, sl, t, tb);
     {
       const R sc = a.pp_kind == OLSB_PP_SCALE ? inv_n * a.pp_c : inv_n;
 #pragma unroll
@@ -800,16 +685,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
       tmem_wait_st();
     }
 
-    for (int f = f_lo; f < f_hi; ++f, ++hseq) {
-      const int slot = int(hseq & 1u);
+    for (int f = f_lo; f < f_hi; ++f) {
       const int f_next = f + 1 < f_hi ? f + 1 : f_next_item;
-      if constexpr (C::HM == H_TMA) {
-        if constexpr (P == 1) __syncthreads();  // no exchange barrier below
-        // prefetch the next (item, filter) pair into the other slot; its
-        // previous contents were consumed before the last exchange barrier
-        if (tid == 0 && f_next >= 0) issue(f_next, slot ^ 1);
-        if constexpr (P == 1) mbar_wait(&hbar[slot], (hseq >> 1) & 1u);
-      }
       // ---- pointwise multiply, both operands bit-reversed
       // (_kernels_nb.py:280-282)
       Cpx<R> y[E];
@@ -825,26 +702,12 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
           mulh(u, hn[u]);
         });
         if (f_next >= 0) fetch(f_next);
-      } else if constexpr (C::HM == H_TMA) {
-        const float4* hs =
-            reinterpret_cast<const float4*>(hbuf + size_t(slot) * G::N) + t;
-        sfor<0, C::VPT>([&](auto uc) {
-          constexpr int u = decltype(uc)::value;
-          mulh(u, hs[u * T]);
-        });
       } else if constexpr (C::HM == H_TEX) {
         const int hb = f * (C::VPT * T) + t;
         sfor<0, C::VPT>([&](auto uc) {
           constexpr int u = decltype(uc)::value;
           mulh(u, tex1Dfetch<float4>(a.htex, hb + u * T));
         });
-      } else if constexpr (C::HM == H_ASYNC) {
-        cp_async_wait_all();
-        sfor<0, C::VPT>([&](auto uc) {
-          constexpr int u = decltype(uc)::value;
-          mulh(u, hpriv[u * C::THREADS]);
-        });
-        if (f_next >= 0) prefetch(f_next);
       } else {
         const typename V16<R>::type* hs = a.spec + (size_t(f) * C::VPT) * T + t;
         sfor<0, C::VPT>([&](auto uc) {
@@ -859,29 +722,15 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
       }
       // ---- inverse FFT (dit_inv, _kernels_nb.py:31-51)
       dit_pass_static<R, C::LOGE, G::G0>(y);
-      auto wait_next = [&]() {
-        if constexpr (C::HM == H_TMA) {
-          if (tid == 0 && f_next >= 0)
-            mbar_wait(&hbar[slot ^ 1], ((hseq + 1) >> 1) & 1u);
-        }
-      };
       sfor<1, P>([&](auto qc) {
         constexpr int q = decltype(qc)::value;
-        if constexpr (q == P - 1) {
-          exchange<C, q - 1, q>(bufs, xc, sl, t, y, wait_next, NoHook{},
-                                IC<C::ABL>{});
-        } else {
-          exchange<C, q - 1, q>(bufs, xc, sl, t, y, NoHook{}, NoHook{},
-                                IC<C::ABL>{});
-        }
+        exchange<C, q - 1, q>(bufs, xc, sl, t, y, IC<C::ABL>{});
         if constexpr (C::TMX && (q == P - 1 || (q == P - 2 && C::TMX == 2))) {
           Tw<R> tw[16];
           tmem_ld_tw(tb + (q == P - 1 ? 32u : 64u), tw);
           dit_pass_rt<R, G::tan01(q)>(y, TwRegs<R>{tw}, top_bits<LOGN, q>(t));
         } else if constexpr (q == P - 1 && C::TOPREG) {
           dit_pass_rt<R, G::tan01(q)>(y, TwRegs<R>{twr}, top_bits<LOGN, q>(t));
-        } else if constexpr (q == P - 2 && C::MIDREG) {
-          dit_pass_rt<R, G::tan01(q)>(y, TwRegs<R>{twm}, top_bits<LOGN, q>(t));
         } else {
           dit_pass_rt<R, G::tan01(q)>(
               y, tw_smem<R, LOGN, q>(lowtab + G::tw_offset(q), t),
@@ -1020,7 +869,7 @@ __global__ void __launch_bounds__(C::THREADS)
     }
     // every load of the group precedes any store (in-place safety)
     __syncthreads();
-    forward_fft<C, false>(x, tab, nullptr, nullptr, bufs, xc, sl, t);
+    forward_fft<C, false>(x, tab, nullptr, bufs, xc, sl, t);
     if (live) {
       if (a.out_perm) {
         Cpx<R>* o = a.out_perm + size_t(r) * G::N + G::thread_part(0, t);

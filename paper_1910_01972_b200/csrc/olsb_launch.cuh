@@ -64,7 +64,7 @@ struct DefaultPolicy {
   static constexpr int SEGS = dbl ? std::max(1, 256 / T) : std::max(1, 128 / T);
   using type = KCfg<R, LOGN, SEGS, (!dbl && LOGN == 12) ? 2 : 1,
                     dbl ? H_LDG : H_TEX, 0,
-                    dbl ? 1 : std::max(1, 512 / (SEGS * T)), 0, dbl ? 0 : 2,
+                    dbl ? 1 : std::max(1, 512 / (SEGS * T)), dbl ? 0 : 2,
                     dbl ? 0 : 1>;
 };
 
@@ -74,16 +74,16 @@ struct DefaultPolicy {
 template <int LOGN, int V>
 struct Variant {
   static constexpr int T = Geo<LOGN>::T;
-  // {SEGS, NBUF, HM, BAR, MINB (warpgroups/SM), MIDREG, TMX, PREF, ABL}
-  static constexpr int tab[8][9] = {
-      {1, 1, H_TEX, 0, 4, 0, 0, 0, 0}, {1, 1, H_TEX, 0, 4, 0, 1, 1, 0},
-      {1, 1, H_TEX, 0, 4, 0, 2, 1, 0}, {1, 2, H_TEX, 0, 4, 0, 2, 1, 0},
-      {1, 1, H_TEX, 0, 4, 0, 2, 1, 1}, {1, 1, H_TEX, 0, 4, 0, 2, 1, 6},
-      {1, 1, H_TEX, 0, 4, 0, 2, 1, 8}, {1, 1, H_TEX, 0, 4, 0, 2, 1, 14}};
+  // {SEGS, NBUF, HM, BAR, MINB (warpgroups/SM), TMX, PREF, ABL}
+  static constexpr int tab[8][8] = {
+      {1, 1, H_TEX, 0, 4, 0, 0, 0}, {1, 1, H_TEX, 0, 4, 1, 1, 0},
+      {1, 1, H_TEX, 0, 4, 2, 1, 0}, {1, 2, H_TEX, 0, 4, 2, 1, 0},
+      {1, 1, H_TEX, 0, 4, 2, 1, 1}, {1, 1, H_TEX, 0, 4, 2, 1, 6},
+      {1, 1, H_TEX, 0, 4, 2, 1, 8}, {1, 1, H_TEX, 0, 4, 2, 1, 14}};
   static constexpr int segs = tab[V][0] * std::max(1, 128 / T);
   static constexpr int minb = std::max(1, tab[V][4] * 128 / (segs * T));
   using type = KCfg<float, LOGN, segs, tab[V][1], tab[V][2], tab[V][3], minb,
-                    tab[V][5], tab[V][6], tab[V][7], tab[V][8]>;
+                    tab[V][5], tab[V][6], tab[V][7]>;
 };
 
 inline int debug_env() {

@@ -164,3 +164,41 @@ def test_sharded_outputs_bit_identical(oc, mode):
             xl = sig.samples[sh.x_lo:sh.x_hi].clone()   # only this rank's data
             got[:, sh.g_lo:sh.g_hi] = convolve_shard(xl, sh, p, fs)
         assert torch.equal(got, full), world
+
+
+_VARIANT_SCRIPT = r"""
+import sys, numpy as np
+sys.path[:0] = [{root!r}, {golden!r}]
+import paper_1910_01972_b200 as oc
+from cases import CONV_GRID, conv_case_inputs
+g = np.load({npz!r})
+worst = 0.0
+for case in (12, 13, 17, 18, 19):
+    ns, m, nfil, n, origin, _ = CONV_GRID[case]
+    x, taps = conv_case_inputs(case)
+    P = oc.Precision.single
+    y = oc.convolve(oc.make_signal(x, "complex", P),
+                    oc.make_filterset(taps, origin, P),
+                    oc.plan(ns, m, "c2c", origin, n)).cpu().numpy()
+    ref = g[f"y_double_{{case}}"]
+    e = np.max(np.linalg.norm(y - ref, axis=1) / np.linalg.norm(ref, axis=1))
+    worst = max(worst, e)
+print(worst)
+"""
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+def test_tuning_variants_correct(variant):
+    # the OLSB_VARIANT kernel policies (tuning sweeps) produce correct results
+    # (variants 4-7 are ablations and intentionally wrong)
+    import os
+    import subprocess
+    import sys
+    from conftest import GOLDEN, ROOT
+    code = _VARIANT_SCRIPT.format(root=ROOT, golden=GOLDEN,
+                                  npz=os.path.join(GOLDEN, "conv_cases.npz"))
+    env = dict(os.environ, OLSB_VARIANT=str(variant))
+    res = subprocess.run([sys.executable, "-c", code], env=env,
+                         capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    assert float(res.stdout.strip().splitlines()[-1]) <= L2_TOL
