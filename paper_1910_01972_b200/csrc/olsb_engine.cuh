@@ -203,20 +203,65 @@ __device__ __forceinline__ void smem_load(const Cpx<typename C::R>* __restrict__
 // twiddle tables for windows 1..P-1 (double-precision math, rounded once).
 // Window q's table goes to lowtab + tw_offset(q), except the top window's
 // when `toptab` is given.
+// Device-wide copy of every runtime-window table of length 2^LOGN, in the
+// canonical layout (window q at tw_offset(q)); filled once per device by
+// tw_table_kernel, which then raises g_twready.  Static device memory: the
+// C ABI never allocates.
+template <int LOGN>
+struct TwTableSize {
+  static constexpr int n = Geo<LOGN>::tw_total() > 0 ? Geo<LOGN>::tw_total() : 1;
+};
+template <class R, int LOGN>
+__device__ Tw<R> g_twtab[TwTableSize<LOGN>::n];
+template <class R, int LOGN>
+__device__ int g_twready;
+
+template <class R, int LOGN>
+__device__ __forceinline__ Tw<R> twiddle_value(int q_lo, int i, bool tan01) {
+  int idx, l;
+  twiddle_decode(q_lo, i, &idx, &l);
+  double c, t;
+  twiddle_entry(q_lo, idx, l, tan01, &c, &t);
+  return Tw<R>{R(c), R(t)};
+}
+
+template <class R, int LOGN>
+__global__ void tw_table_kernel() {
+  using G = Geo<LOGN>;
+  sfor<1, G::P>([&](auto qc) {
+    constexpr int q = decltype(qc)::value;
+    for (int i = threadIdx.x; i < G::tw_entries(q); i += blockDim.x)
+      g_twtab<R, LOGN>[G::tw_offset(q) + i] =
+          twiddle_value<R, LOGN>(G::lo(q), i, G::tan01(q));
+  });
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) atomicExch(&g_twready<R, LOGN>, 1);
+}
+
+// twiddle tables for windows 1..P-1 (double-precision math, rounded once).
+// Window q's table goes to lowtab + tw_offset(q), except the top window's
+// when `toptab` is given.  Copied from the device-wide table once it is
+// ready, else computed here (same values bit for bit).
 template <class R, int LOGN>
 __device__ void build_tables(Tw<R>* lowtab, Tw<R>* toptab) {
   using G = Geo<LOGN>;
+  int ready;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];"
+               : "=r"(ready)
+               : "l"(&g_twready<R, LOGN>)
+               : "memory");
   sfor<1, G::P>([&](auto qc) {
     constexpr int q = decltype(qc)::value;
     constexpr int lo = G::lo(q);
     constexpr int cnt = G::tw_entries(q);
     Tw<R>* dst = (q == G::P - 1 && toptab) ? toptab : lowtab + G::tw_offset(q);
-    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-      int idx, l;
-      twiddle_decode(lo, i, &idx, &l);
-      double c, t;
-      twiddle_entry(lo, idx, l, G::tan01(q), &c, &t);
-      dst[i] = Tw<R>{R(c), R(t)};
+    if (ready) {
+      const Tw<R>* src = g_twtab<R, LOGN> + G::tw_offset(q);
+      for (int i = threadIdx.x; i < cnt; i += blockDim.x) dst[i] = src[i];
+    } else {
+      for (int i = threadIdx.x; i < cnt; i += blockDim.x)
+        dst[i] = twiddle_value<R, LOGN>(lo, i, G::tan01(q));
     }
   });
 }

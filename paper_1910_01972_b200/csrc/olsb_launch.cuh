@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 
@@ -102,8 +103,24 @@ inline int variant_env() {
   return v;
 }
 
+// Fill the device-wide twiddle table of (R, LOGN) once per device, on the
+// caller's stream (kernels that run before it completes compute their own).
+template <class R, int LOGN>
+int ensure_twiddle_table(cudaStream_t st) {
+  constexpr int kMaxDev = 64;
+  static std::atomic<int> filled[kMaxDev];
+  if (Geo<LOGN>::tw_total() == 0) return 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDev) return 0;
+  if (filled[dev].exchange(1) == 1) return 0;
+  tw_table_kernel<R, LOGN><<<1, 1024, 0, st>>>();
+  return int(cudaGetLastError());
+}
+
 template <class C, int MODE = FMODE_C2C>
 int launch_fused_cfg(FusedArgs<typename C::R> a, cudaStream_t st) {
+  if (int rc = ensure_twiddle_table<typename C::R, C::LOGN>(st)) return rc;
   auto kern = fused_c2c_kernel<C, MODE>;
   int resident = 0;
   int rc = prepare(kern, C::f_smem_bytes, C::THREADS, &resident);

@@ -202,3 +202,40 @@ def test_tuning_variants_correct(variant):
                          capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stderr[-2000:]
     assert float(res.stdout.strip().splitlines()[-1]) <= L2_TOL
+
+
+@pytest.mark.parametrize("mode,ppk", [("c2c", "none"), ("c2c", "scale"),
+                                      ("c2c", "magnitude_squared"),
+                                      ("c2c", "derivative"), ("r2r", "none"),
+                                      ("r2r", "derivative")])
+def test_executor_and_graph_replay_bit_identical(oc, mode, ppk):
+    ns, m, nfil, n, origin = 30000, 129, 3, 1024, 5
+    rng = np.random.default_rng([70, ns])
+    real = mode == "r2r"
+    x = rng.standard_normal(ns) if real else (rng.standard_normal(ns)
+                                              + 1j * rng.standard_normal(ns))
+    taps = rng.standard_normal((nfil, m)) if real else (
+        rng.standard_normal((nfil, m)) + 1j * rng.standard_normal((nfil, m)))
+    P = oc.Precision.single
+    p = oc.plan(ns, m, mode, origin, n)
+    pp = oc.PostProcSpec(ppk, 0.5 if ppk == "scale" else 1.0)
+    fs = oc.make_filterset(taps, origin, P)
+    sig = oc.make_signal(x, "real" if real else "complex", P)
+    ref = oc.convolve(sig, fs, p, postproc=pp)
+    ex = oc.Executor(fs, p, pp)
+    assert torch.equal(ex(sig), ref)
+    out = torch.empty_like(ref)
+    xs = sig.samples.clone()
+    run = ex.graph(xs, out)
+    run()
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
+    # new data through the same captured graph
+    xs.mul_(2)
+    run()
+    torch.cuda.synchronize()
+    want = oc.convolve(oc.make_signal(xs, "real" if real else "complex", P), fs,
+                       p, postproc=pp)
+    assert torch.equal(out, want)
+    with pytest.raises(ValueError):
+        ex(sig.samples[:-1])

@@ -55,6 +55,16 @@ for ns, m, nfil, n in [(1 << 20, 64, 1, 1024), (1 << 16, 64, 4, 256)]:
     e1.record()
     e1.synchronize()
     graph_us = e0.elapsed_time(e1) / 20 * 1e3
+    ex = ob.Executor(fs, p)
+    for _ in range(20):
+        ex(sig, out)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        ex(sig, out)
+    torch.cuda.synchronize()
+    ex_us = (time.perf_counter() - t0) / reps * 1e6
     print(f"ns={ns} m={m} F={nfil} N={n}: convolve() host {host_us:.1f} us/call, "
+          f"Executor host {ex_us:.1f} us/call, "
           f"graph-replayed kernel {graph_us:.1f} us, traffic at HBM peak "
           f"{8 * ns * (1 + nfil) / 6.546e12 * 1e6:.1f} us", flush=True)
