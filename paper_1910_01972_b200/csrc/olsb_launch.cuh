@@ -58,13 +58,15 @@ template <class R, int LOGN>
 struct DefaultPolicy {
   static constexpr bool dbl = std::is_same<R, double>::value;
   static constexpr int T = Geo<LOGN>::T;
-  // fp32 (OLSB_VARIANT=2 / 3 of the sweep in DESIGN.md §5): 128-thread CTAs,
+  // fp32 (OLSB_VARIANT=2 / 3 of the sweep in DESIGN.md §5, plus BAR = 1): 128-thread CTAs,
   // 4 CTAs per SM, segment spectrum and runtime-window twiddles in TMEM, the
   // next filter's spectrum prefetched through the TEX path; N = 4096 double
   // buffers the exchange (one barrier per exchange).
   static constexpr int SEGS = dbl ? std::max(1, 256 / T) : std::max(1, 128 / T);
+  // BAR = 1: named barrier per segment group, so only the warps of one
+  // segment are coupled (matters for N = 1024: two 2-warp groups per CTA)
   using type = KCfg<R, LOGN, SEGS, (!dbl && LOGN == 12) ? 2 : 1,
-                    dbl ? H_LDG : H_TEX, 0,
+                    dbl ? H_LDG : H_TEX, 1,
                     dbl ? 1 : std::max(1, 512 / (SEGS * T)), dbl ? 0 : 2,
                     dbl ? 0 : 1>;
 };
