@@ -266,6 +266,53 @@ __device__ void build_tables(Tw<R>* lowtab, Tw<R>* toptab) {
   });
 }
 
+// ---- predicated read-only loads (zero when !ok): branch-free, so all loads
+// of a segment window are in flight together
+__device__ __forceinline__ Cpx<float> ld_nc_or0(const Cpx<float>* p, bool ok) {
+  float re, im;
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n"
+      " mov.b32 %0, 0;\n mov.b32 %1, 0;\n"
+      " @q ld.global.nc.v2.f32 {%0, %1}, [%2];\n}"
+      : "=f"(re), "=f"(im)
+      : "l"(p), "r"(int(ok)));
+  return Cpx<float>{re, im};
+}
+__device__ __forceinline__ Cpx<double> ld_nc_or0(const Cpx<double>* p, bool ok) {
+  double re, im;
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n"
+      " mov.b64 %0, 0;\n mov.b64 %1, 0;\n"
+      " @q ld.global.nc.v2.f64 {%0, %1}, [%2];\n}"
+      : "=d"(re), "=d"(im)
+      : "l"(p), "r"(int(ok)));
+  return Cpx<double>{re, im};
+}
+__device__ __forceinline__ float ld_nc_or0(const float* p, bool ok) {
+  float v;
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n mov.b32 %0, 0;\n"
+      " @q ld.global.nc.f32 %0, [%1];\n}"
+      : "=f"(v)
+      : "l"(p), "r"(int(ok)));
+  return v;
+}
+__device__ __forceinline__ double ld_nc_or0(const double* p, bool ok) {
+  double v;
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n mov.b64 %0, 0;\n"
+      " @q ld.global.nc.f64 %0, [%1];\n}"
+      : "=d"(v)
+      : "l"(p), "r"(int(ok)));
+  return v;
+}
+
+// ---- TMA prefetch of a global range into L2 (16-byte aligned / sized)
+__device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes)
+               : "memory");
+}
+
 // ---- shared-memory address for PTX operands
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -674,6 +721,34 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     const unsigned vmask_b =
         MODE == FMODE_R2R ? seg_mask(g0 + a.seg_len, o_lo_b, span_b) : 0u;
     const long long w0 = g0 - a.t0 + a.origin;
+    // L2 prefetch of the next item's input window (TMA, one thread): with
+    // few filters per segment nothing else hides the DRAM latency of the
+    // gather at the start of an item
+    if (tid == 0 && it + gridDim.x < nitems) {
+      const long long gn = (it + gridDim.x) / nfch;
+      const long long sn = a.k_lo + gn * C::SEGS;
+      const long long segs = MODE == FMODE_R2R ? 2 * C::SEGS : C::SEGS;
+      long long lo = (MODE == FMODE_R2R ? 2 * sn : sn) * a.seg_len - a.t0 + a.origin;
+      long long hi = lo + (segs - 1) * a.seg_len + G::N;
+      lo = lo > 0 ? lo : 0;
+      hi = hi < a.n_s ? hi : a.n_s;
+      const int esz = MODE == FMODE_R2R ? int(sizeof(R)) : int(sizeof(Cpx<R>));
+      if (hi > lo) {
+        const char* base = MODE == FMODE_R2R
+                               ? reinterpret_cast<const char*>(a.xr)
+                               : reinterpret_cast<const char*>(a.x);
+        uintptr_t b0 = reinterpret_cast<uintptr_t>(base + (lo - a.x_base) * esz);
+        uintptr_t b1 = reinterpret_cast<uintptr_t>(base + (hi - a.x_base) * esz);
+        b0 &= ~uintptr_t(15);
+        b1 = (b1 + 15) & ~uintptr_t(15);
+        // stay inside the caller's buffer: whole 16-byte units only
+        if (b1 > reinterpret_cast<uintptr_t>(base + (hi - a.x_base) * esz))
+          b1 -= 16;
+        if (b0 < reinterpret_cast<uintptr_t>(base + (lo - a.x_base) * esz))
+          b0 += 16;
+        if (b1 > b0) l2_prefetch(reinterpret_cast<const void*>(b0), uint32_t(b1 - b0));
+      }
+    }
     const int f_lo = fc * a.fchunk;
     const int f_hi = min(a.n_fil, f_lo + a.fchunk);
     const long long nit = it + gridDim.x;
@@ -696,10 +771,10 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
         constexpr int e = decltype(ec)::value;
         const long long ga = pa + G::elem_part(q, e);
         const long long gb = pbb + G::elem_part(q, e);
-        const R ra = (la && (unsigned long long)ga < (unsigned long long)a.n_s)
-                         ? a.xr[ga - a.x_base] : R(0);
-        const R rb = (lb && (unsigned long long)gb < (unsigned long long)a.n_s)
-                         ? a.xr[gb - a.x_base] : R(0);
+        const R ra = ld_nc_or0(a.xr + (ga - a.x_base),
+                               la && (unsigned long long)ga < (unsigned long long)a.n_s);
+        const R rb = ld_nc_or0(a.xr + (gb - a.x_base),
+                               lb && (unsigned long long)gb < (unsigned long long)a.n_s);
         x[e] = Cpx<R>{ra, rb};
       });
     } else {
@@ -709,11 +784,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
       sfor<0, E>([&](auto ec) {
         constexpr int e = decltype(ec)::value;
         const long long gi = pb + G::elem_part(q, e);
-        if (live && (unsigned long long)gi < (unsigned long long)a.n_s) {
-          x[e] = xp[G::elem_part(q, e)];
-        } else {
-          x[e] = Cpx<R>{R(0), R(0)};
-        }
+        x[e] = ld_nc_or0(xp + G::elem_part(q, e),
+                         live && (unsigned long long)gi < (unsigned long long)a.n_s);
       });
     }
     // ---- forward FFT (dif_fwd, _kernels_nb.py:11-28); the spectrum stays in

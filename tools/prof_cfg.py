@@ -24,6 +24,11 @@ CFG = {
     "cfg2_n4096": (1 << 22, 1024, 32, 4096),
     "cfg4_m8_f8": (1 << 24, 8, 8, 64),
     "cfg4_m32_f8": (1 << 24, 32, 8, 128),
+    "cfg4_m8_f1": (1 << 24, 8, 1, 64),
+    "cfg4_m16_f1": (1 << 24, 16, 1, 64),
+    "cfg4_m32_f1": (1 << 24, 32, 1, 128),
+    "cfg4_m16_f8": (1 << 24, 16, 8, 64),
+    "cfg4_m8_f4": (1 << 24, 8, 4, 64),
     # cfg5's per-GPU share at 8 GPUs (2^30 / 8 samples, 64 filters M=512)
     "cfg5_shard8": (1 << 27, 512, 64, 4096),
     # real (r2r) path on the same shapes
