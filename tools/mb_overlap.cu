@@ -15,8 +15,8 @@ __device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
 template <int MODE, int K>
 __global__ void __launch_bounds__(128, 4) k(float2* out, long long rows, int row_len) {
   // a "row" = one (segment, filter): 128 threads x 16 samples
-  u64 acc[8];
-  for (int i = 0; i < 8; ++i) acc[i] = threadIdx.x + i;
+  u64 acc[8], acc2[8];
+  for (int i = 0; i < 8; ++i) { acc[i] = threadIdx.x + i; acc2[i] = threadIdx.x * 3 + i; }
   const u64 s = 0x3f8000003f800000ull;
   for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
     if (MODE & 1) {
@@ -24,6 +24,15 @@ __global__ void __launch_bounds__(128, 4) k(float2* out, long long rows, int row
       for (int it = 0; it < K / 8; ++it)
 #pragma unroll
         for (int i = 0; i < 8; ++i) acc[i] = fma2(acc[i], s, acc[(i + 1) & 7]);
+    }
+    if (MODE & 4) {  // pipe-bound FP: 16 independent chains
+#pragma unroll 1
+      for (int it = 0; it < K / 16; ++it)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          acc[i] = fma2(acc[i], s, s);
+          acc2[i] = fma2(acc2[i], s, s);
+        }
     }
     if (MODE & 2) {
       float2* p = out + r * (long long)row_len + threadIdx.x;
@@ -34,7 +43,7 @@ __global__ void __launch_bounds__(128, 4) k(float2* out, long long rows, int row
       }
     }
   }
-  if (acc[0] == 12345) out[0] = make_float2(1, 1);
+  if (acc[0] == 12345 || acc2[3] == 777) out[0] = make_float2(1, 1);
 }
 int main() {
   int sms;
@@ -62,5 +71,9 @@ int main() {
   run("fp+store  K=280", k<3, 280>);
   run("fp only   K=200", k<1, 200>);
   run("fp+store  K=200", k<3, 200>);
+  run("ILP fp only K=1600", k<4, 1600>);
+  run("ILP fp+store K=1600", k<6, 1600>);
+  run("ILP fp only K=2400", k<4, 2400>);
+  run("ILP fp+store K=2400", k<6, 2400>);
   return 0;
 }
