@@ -18,6 +18,8 @@ conv_cases.npz     convolve(variant="fused") c2c (ols.py:257-360) on a grid of
                    last segment, M=1, M=N, N_s < L, origin > 0, real taps.
 pp_cases.npz       the real (r2r) path and the magnitude_squared epilogue
                    (fused_r2r / fused_c2c_abs2) on a grid of small cells.
+io/                OLS1 binary / text sample files written by the reference's
+                   io.write_samples (CLI file-format compatibility).
 cfg_windows.npz    BASELINE.json configs 1-4 at FULL size: float64 reference
                    output on fixed windows + per-filter checksums.  Inputs are
                    regenerated anywhere from the reference's own generator
@@ -121,6 +123,26 @@ def pp_fixtures():
     np.savez_compressed(os.path.join(HERE, "pp_cases.npz"), **out)
 
 
+def io_fixtures():
+    """OLS1 binary and text sample files written by the reference's own
+    writer (io.py), for byte-level compatibility tests."""
+    from olsconv.io import write_samples
+    d = os.path.join(HERE, "io")
+    os.makedirs(d, exist_ok=True)
+    rng = np.random.default_rng([90])
+    arrays = {
+        "real_single": rng.standard_normal(37).astype(np.float32),
+        "real_double": rng.standard_normal(5),
+        "complex_single": (rng.standard_normal(11)
+                           + 1j * rng.standard_normal(11)).astype(np.complex64),
+        "complex_double": rng.standard_normal(4) + 1j * rng.standard_normal(4),
+    }
+    for name, arr in arrays.items():
+        write_samples(os.path.join(d, f"{name}.bin"), arr)
+        write_samples(os.path.join(d, f"{name}.txt"), arr)
+    np.savez_compressed(os.path.join(d, "arrays.npz"), **arrays)
+
+
 def cfg_fixtures():
     out = {}
     for name, ns, m, nfil, n in CFGS:
@@ -143,7 +165,7 @@ def cfg_fixtures():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["fft", "spectra", "conv", "pp", "cfg"]
+    which = sys.argv[1:] or ["fft", "spectra", "conv", "pp", "io", "cfg"]
     if "fft" in which:
         fft_fixtures()
     if "spectra" in which:
@@ -152,6 +174,8 @@ if __name__ == "__main__":
         conv_fixtures()
     if "pp" in which:
         pp_fixtures()
+    if "io" in which:
+        io_fixtures()
     if "cfg" in which:
         cfg_fixtures()
     print("backend:", oc.backend_name())
