@@ -52,7 +52,7 @@ enum HMode : int {
 // barrier scope (0: CTA-wide __syncthreads, 1: named barrier per group),
 // MINB target CTAs per SM (register cap).
 template <class R_, int LOGN_, int SEGS_, int NBUF_, int HM_, int BAR_,
-          int MINB_, int TMX_ = 0, int PREF_ = 0, int ABL_ = 0>
+          int MINB_, int TMX_ = 0, int PREF_ = 0, int ABL_ = 0, int MB_ = 0>
 struct KCfg {
   using R = R_;
   static constexpr int LOGN = LOGN_;
@@ -94,6 +94,10 @@ struct KCfg {
   // exchanges, 4 no inverse exchange barriers, 8 spectra of filters f & 1
   // only (L1-resident: isolates the L2 traffic of the spectrum fetches)
   static constexpr int ABL = ABL_;
+  // MB: the "buffer free" side of each exchange is an mbarrier per segment
+  // group (every warp arrives after its loads; the next exchange's stores
+  // wait on that phase) instead of a blocking barrier before the stores
+  static constexpr bool MB = MB_ && NBUF_ == 1 && T > 32 && !(ABL_ & 4);
   static constexpr bool TOPREG = !dbl && P >= 2 && !TMX;
   // the top window's table is built in the exchange buffers (TOPREG / TMX)
   static constexpr bool TOPOUT = TOPREG || TMX;
@@ -114,8 +118,9 @@ struct KCfg {
   static constexpr size_t f_tab_off = f_bufs_bytes;
   static constexpr size_t f_tab_bytes = al(size_t(lowtab_elems) * sizeof(Tw<R>));
   static constexpr size_t f_slot_off = f_tab_off + f_tab_bytes;
-  // [TMEM base address slot]
-  static constexpr size_t f_smem_bytes = f_slot_off + 16;
+  // [TMEM base address slot | MB: one mbarrier per segment group]
+  static constexpr size_t f_mbar_off = f_slot_off + 16;
+  static constexpr size_t f_smem_bytes = f_mbar_off + (MB ? 8 * SEGS : 0);
 };
 
 // configuration of the row kernels (filter spectra, standalone transforms)
@@ -139,6 +144,32 @@ __device__ __forceinline__ void group_sync(int sl) {
   } else {
     __syncthreads();
   }
+}
+
+// mbarrier helpers (MB exchanges)
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+template <class C>
+__device__ __forceinline__ uint32_t group_mbar(int sl) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  return uint32_t(__cvta_generic_to_shared(smem_raw + C::f_mbar_off)) + 8u * sl;
 }
 
 // ---------------------------------------------------------------------------
@@ -500,7 +531,12 @@ __device__ __forceinline__ void exchange(Cpx<typename C::R>* bufs, int& xc,
   // stores stays group-wide: the buffer's previous user may be a cross-warp
   // exchange whose loads other warps are still issuing.
   constexpr bool WL = C::G::warp_local(X);
-  if constexpr (C::NBUF == 1 && !(ABL & 4)) group_sync<C>(sl);
+  if constexpr (C::MB) {
+    // the previous exchange's loads are done in every warp of the group
+    if (xc > 0) mbar_wait(group_mbar<C>(sl), uint32_t(xc - 1) & 1u);
+  } else if constexpr (C::NBUF == 1 && !(ABL & 4)) {
+    group_sync<C>(sl);
+  }
   if constexpr (!(ABL & 2)) smem_store<C, QW, X>(buf, t, x);
   if constexpr (!(ABL & 4)) {
     if constexpr (WL) {
@@ -510,6 +546,10 @@ __device__ __forceinline__ void exchange(Cpx<typename C::R>* bufs, int& xc,
     }
   }
   if constexpr (!(ABL & 2)) smem_load<C, QR, X>(buf, t, x);
+  if constexpr (C::MB) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(group_mbar<C>(sl));
+  }
   ++xc;
 }
 
@@ -628,6 +668,9 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   }
   build_tables<R, LOGN>(lowtab,
                         C::TOPOUT ? reinterpret_cast<Tw<R>*>(bufs) : nullptr);
+  if constexpr (C::MB) {
+    if (tid < C::SEGS) mbar_init(group_mbar<C>(tid), T / 32);
+  }
   __syncthreads();
   uint32_t tbase = 0, tb = 0;
   if constexpr (C::TMX) {
@@ -901,7 +944,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
               y[e] = Cpx<R>{dv(g, l.re, y[e].re, r.re),
                             dv(gi, l.im, y[e].im, r.im)};
             });
-            if constexpr (C::NBUF == 2) group_sync<C>(sl);  // next exchange
+            if constexpr (C::NBUF == 2 || C::MB) group_sync<C>(sl);  // next exchange
           }
         }
       }

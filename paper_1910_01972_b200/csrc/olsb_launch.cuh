@@ -65,10 +65,12 @@ struct DefaultPolicy {
   static constexpr int SEGS = dbl ? std::max(1, 256 / T) : std::max(1, 128 / T);
   // BAR = 1: named barrier per segment group, so only the warps of one
   // segment are coupled (matters for N = 1024: two 2-warp groups per CTA)
+  // N = 1024 (two 2-warp groups per CTA): mbarrier "buffer free" exchanges
+  // (OLSB_VARIANT=8 in the sweep: 0.317 vs 0.330 ms on cfg2; slower at 2048)
   using type = KCfg<R, LOGN, SEGS, (!dbl && LOGN == 12) ? 2 : 1,
                     dbl ? H_LDG : H_TEX, 1,
                     dbl ? 1 : std::max(1, 512 / (SEGS * T)), dbl ? 0 : 2,
-                    dbl ? 0 : 1>;
+                    dbl ? 0 : 1, 0, (!dbl && LOGN == 10) ? 1 : 0>;
 };
 
 // tuning variants for fp32 (OLSB_VARIANT).  A CTA holds SEGS x max(1,
@@ -77,16 +79,17 @@ struct DefaultPolicy {
 template <int LOGN, int V>
 struct Variant {
   static constexpr int T = Geo<LOGN>::T;
-  // {SEGS, NBUF, HM, BAR, MINB (warpgroups/SM), TMX, PREF, ABL}
-  static constexpr int tab[8][8] = {
-      {1, 1, H_TEX, 0, 4, 0, 0, 0}, {1, 1, H_TEX, 0, 4, 1, 1, 0},
-      {1, 1, H_TEX, 0, 4, 2, 1, 0}, {1, 2, H_TEX, 0, 4, 2, 1, 0},
-      {1, 1, H_TEX, 0, 4, 2, 1, 1}, {1, 1, H_TEX, 0, 4, 2, 1, 6},
-      {1, 1, H_TEX, 0, 4, 2, 1, 8}, {1, 1, H_TEX, 0, 4, 2, 1, 14}};
+  // {SEGS, NBUF, HM, BAR, MINB (warpgroups/SM), TMX, PREF, ABL, MB}
+  static constexpr int tab[9][9] = {
+      {1, 1, H_TEX, 0, 4, 0, 0, 0, 0}, {1, 1, H_TEX, 0, 4, 1, 1, 0, 0},
+      {1, 1, H_TEX, 0, 4, 2, 1, 0, 0}, {1, 2, H_TEX, 0, 4, 2, 1, 0, 0},
+      {1, 1, H_TEX, 0, 4, 2, 1, 1, 0}, {1, 1, H_TEX, 0, 4, 2, 1, 6, 0},
+      {1, 1, H_TEX, 0, 4, 2, 1, 8, 0}, {1, 1, H_TEX, 0, 4, 2, 1, 14, 0},
+      {1, 1, H_TEX, 1, 4, 2, 1, 0, 1}};
   static constexpr int segs = tab[V][0] * std::max(1, 128 / T);
   static constexpr int minb = std::max(1, tab[V][4] * 128 / (segs * T));
   using type = KCfg<float, LOGN, segs, tab[V][1], tab[V][2], tab[V][3], minb,
-                    tab[V][5], tab[V][6], tab[V][7]>;
+                    tab[V][5], tab[V][6], tab[V][7], tab[V][8]>;
 };
 
 inline int debug_env() {
@@ -160,6 +163,7 @@ int launch_fused(FusedArgs<R> a, int mode, cudaStream_t st) {
       case 5: return launch_fused_cfg<typename Variant<LOGN, 5>::type>(a, st);
       case 6: return launch_fused_cfg<typename Variant<LOGN, 6>::type>(a, st);
       case 7: return launch_fused_cfg<typename Variant<LOGN, 7>::type>(a, st);
+      case 8: return launch_fused_cfg<typename Variant<LOGN, 8>::type>(a, st);
       default: break;
     }
   }

@@ -187,7 +187,7 @@ print(worst)
 """
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 8])
 def test_tuning_variants_correct(variant):
     # the OLSB_VARIANT kernel policies (tuning sweeps) produce correct results
     # (variants 4-7 are ablations and intentionally wrong)

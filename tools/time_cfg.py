@@ -5,6 +5,7 @@ Prints one line per config; also checks one golden case for parity.
 """
 import os
 import sys
+import time
 
 import numpy as np
 import torch
@@ -35,7 +36,7 @@ def parity():
     return worst
 
 
-def time_cfg(name, reps=20):
+def time_cfg(name, reps=200):
     ns, m, nfil, n, *mode = CFG[name]
     mode = mode[0] if mode else "c2c"
     x, taps = gen_inputs(ns, m, nfil)
@@ -48,18 +49,34 @@ def time_cfg(name, reps=20):
                               "natural" if mode == "r2r" else "permuted")
     out = torch.empty((nfil, ns), dtype=torch.float32 if mode == "r2r"
                       else torch.complex64, device="cuda")
+    # back-to-back launches between two events (the host-side call overhead
+    # overlaps the previous kernel; an event pair around each synchronous
+    # call would count it for cells shorter than ~0.1 ms).  Windows of ~20 ms
+    # with idle gaps: long sustained runs hit the 1000 W power cap and drop
+    # the SM clock (tools/power_probe.py); median of 5 windows
+    ex = ob.Executor(fs, p)
+    xs = sig.samples
     for _ in range(3):
-        ob.convolve(sig, fs, p, out=out)
+        ex(xs, out)
     torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    ex(xs, out)
+    e1.record()
+    e1.synchronize()
+    reps = max(3, min(reps, int(20.0 / max(e0.elapsed_time(e1), 1e-3))))
     ts = []
-    for _ in range(reps):
+    for _ in range(5):
+        time.sleep(0.25)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        ob.convolve(sig, fs, p, out=out)
+        for _ in range(reps):
+            ex(xs, out)
         e1.record()
         e1.synchronize()
-        ts.append(e0.elapsed_time(e1) * 1e-3)
+        ts.append(e0.elapsed_time(e1) * 1e-3 / reps)
     t = float(np.median(ts))
     byts = (4 if mode == "r2r" else 8) * ns * (1 + nfil)
     return t, byts / t / 6546.6e9
