@@ -328,7 +328,7 @@ def main():
                "d2h_bytes_per_step": int(NFIL * n_own * 8),
                "ms_per_step": float(te.item()),
                "path": "make_signal(pinned host) + convolve(out=pinned host)"
-                       " streaming chunks" if world == 1 else
+                       " streaming row chunks (contiguous D2H)" if world == 1 else
                        "per-rank H2D shard + fused_range + D2H"}
 
     # ---- the paper's comparison point: cuFFT-based OLS (Algorithm 1,

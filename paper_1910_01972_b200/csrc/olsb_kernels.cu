@@ -72,7 +72,8 @@ struct TexKey {
   cudaTextureObject_t tex;
 };
 static std::mutex g_tex_mu;
-static TexKey g_tex_cache[64];
+constexpr int kTexCache = 128;
+static TexKey g_tex_cache[kTexCache];
 static int g_tex_n = 0;
 
 int spectra_texture(const void* ptr, size_t bytes,
@@ -99,10 +100,14 @@ int spectra_texture(const void* ptr, size_t bytes,
   if (e != cudaSuccess) return int(e);
   // a freed-and-reused allocation with the same address keeps a valid
   // descriptor (linear textures hold only pointer + size)
-  if (g_tex_n == 64) {
+  if (g_tex_n == kTexCache) {
+    // the oldest object may still be read by a kernel in flight on any
+    // stream: drain the device before destroying it (rare: only after
+    // kTexCache distinct spectra buffers)
+    cudaDeviceSynchronize();
     cudaDestroyTextureObject(g_tex_cache[0].tex);
-    for (int i = 1; i < 64; ++i) g_tex_cache[i - 1] = g_tex_cache[i];
-    g_tex_n = 63;
+    for (int i = 1; i < kTexCache; ++i) g_tex_cache[i - 1] = g_tex_cache[i];
+    g_tex_n = kTexCache - 1;
   }
   g_tex_cache[g_tex_n++] = TexKey{dev, ptr, bytes, tex};
   *out = tex;

@@ -426,17 +426,31 @@ def input_extent(seg_plan: SegmentPlan, g_lo: int, g_hi: int) -> Tuple[int, int]
     return lo.value, hi.value
 
 
+_STREAM_TILE = 256 << 20   # bytes of output per streaming chunk
+
+
 def _fused_streaming(signal, spec_dev, seg_plan, pp, precision, l_eff, t0,
                      win_off, n_seg, out, chunk_segments):
-    """Host-memory path: per chunk of outputs, H2D of its input extent, fused
-    kernel into a device staging tile, strided D2H into ``out``.  Three
-    streams rotate over three staging slots so copies in both directions
-    overlap the kernel of the neighbouring chunks."""
+    """Host-memory path: per chunk of outputs, fused kernel into a device
+    staging tile and D2H into ``out``.  Three streams rotate over three
+    staging slots so copies in both directions overlap the kernel of the
+    neighbouring chunks.  When one output row fits a tile and there are at
+    least three filters, chunks are blocks of whole rows (filters): every D2H
+    is one contiguous copy (~55 GB/s over PCIe against ~51 GB/s for the
+    strided copies of segment chunks) and the signal goes to the device once.
+    Otherwise (or with ``chunk_segments``) chunks are segment ranges with
+    their input extents copied per chunk.  Results are bit-identical either
+    way."""
     n_s = signal.length
     n_fil = spec_dev.shape[0]
+    esize = out.element_size()
+    row = n_s * esize
+    if chunk_segments is None and n_fil >= 3 and row <= _STREAM_TILE:
+        fc = max(1, min(_STREAM_TILE // row, n_fil // 3))
+        return _fused_streaming_rows(signal, spec_dev, seg_plan, pp, precision,
+                                     out, fc)
     x_host = signal.samples
     dev = spec_dev.device
-    esize = out.element_size()
     if chunk_segments is None:
         # ~256 MiB of output per chunk
         chunk_segments = max(1, (256 << 20) // max(1, n_fil * l_eff * esize))
@@ -469,6 +483,44 @@ def _fused_streaming(signal, spec_dev, seg_plan, pp, precision, l_eff, t0,
                     out.data_ptr() + ga * esize, n_s * esize,
                     obuf[k].data_ptr(), w * esize, (gb - ga) * esize,
                     n_fil, 0, st.cuda_stream), "olsb_copy2d_async")
+        for s in streams:
+            ready.wait_stream(s)
+        # keep the staging buffers alive until the copies retire
+        for s in streams:
+            s.synchronize()
+    return out
+
+
+def _fused_streaming_rows(signal, spec_dev, seg_plan, pp, precision, out,
+                          fc):
+    """Host-memory path chunked by filters (see _fused_streaming)."""
+    n_s = signal.length
+    n_fil = spec_dev.shape[0]
+    dev = spec_dev.device
+    chunks = [(f, min(f + fc, n_fil)) for f in range(0, n_fil, fc)]
+    nslot = min(3, len(chunks))
+    with torch.cuda.device(dev):
+        streams = [torch.cuda.Stream() for _ in range(nslot)]
+        ready = torch.cuda.current_stream()
+        for s in streams:
+            s.wait_stream(ready)
+        xdev = torch.empty(n_s, dtype=signal.samples.dtype, device=dev)
+        with torch.cuda.stream(streams[0]):
+            xdev.copy_(signal.samples, non_blocking=True)
+        staged = torch.cuda.Event()
+        staged.record(streams[0])
+        for s in streams[1:]:
+            s.wait_event(staged)
+        obuf = [torch.empty((fc, n_s), dtype=out.dtype, device=dev)
+                for _ in range(nslot)]
+        for i, (f0, f1) in enumerate(chunks):
+            k = i % nslot
+            st = streams[k]
+            with torch.cuda.stream(st):
+                fused_range_launch(xdev, 0, n_s, spec_dev[f0:f1], f1 - f0,
+                                   seg_plan, 0, n_s, pp, obuf[k], n_s, 0,
+                                   precision, st.cuda_stream)
+                out[f0:f1].copy_(obuf[k][:f1 - f0], non_blocking=True)
         for s in streams:
             ready.wait_stream(s)
         # keep the staging buffers alive until the copies retire
