@@ -227,27 +227,33 @@ def test_host_streaming_path_bit_identical(oc):
     assert torch.equal(host_out, dev.cpu())
 
 
-@pytest.mark.parametrize("nfil", [3, 7, 16])
-def test_host_streaming_filter_chunks_bit_identical(oc, nfil):
+@pytest.mark.parametrize("mode,nfil", [("c2c", 3), ("c2c", 7), ("c2c", 16),
+                                       ("r2r", 7)])
+def test_host_streaming_filter_chunks_bit_identical(oc, mode, nfil):
     # default host path: chunks of whole output rows (filters), one
     # contiguous D2H each; ragged last chunk for nfil = 7 / 16
     from paper_1910_01972_b200 import ols as ols_mod
     ns, m, n, origin = 50000, 77, 512, 3
     rng = np.random.default_rng([71, nfil])
-    x = rng.standard_normal(ns) + 1j * rng.standard_normal(ns)
-    taps = rng.standard_normal((nfil, m)) + 1j * rng.standard_normal((nfil, m))
+    real = mode == "r2r"
+    x = rng.standard_normal(ns) + (0 if real else 1j * rng.standard_normal(ns))
+    taps = rng.standard_normal((nfil, m)) + (
+        0 if real else 1j * rng.standard_normal((nfil, m)))
     P = oc.Precision.single
-    p = oc.plan(ns, m, "c2c", origin, n)
-    fs = oc.transform_filters(oc.make_filterset(taps, origin, P), p, "permuted")
-    dev = oc.convolve(oc.make_signal(x, "complex", P), fs, p)
-    hsig = oc.make_signal(torch.from_numpy(x.astype(np.complex64)).pin_memory(),
-                          "complex", P, device="cpu")
-    host_out = torch.full((nfil, ns), float("nan"),
-                          dtype=torch.complex64).pin_memory()
+    kind = "real" if real else "complex"
+    hdt = np.float32 if real else np.complex64
+    tdt = torch.float32 if real else torch.complex64
+    p = oc.plan(ns, m, mode, origin, n)
+    fs = oc.transform_filters(oc.make_filterset(taps, origin, P), p,
+                              "natural" if real else "permuted")
+    dev = oc.convolve(oc.make_signal(x, kind, P), fs, p)
+    hsig = oc.make_signal(torch.from_numpy(x.astype(hdt)).pin_memory(),
+                          kind, P, device="cpu")
+    host_out = torch.full((nfil, ns), float("nan"), dtype=tdt).pin_memory()
     tile = ols_mod._STREAM_TILE
     try:
         # a small tile forces several row chunks (2 rows per chunk)
-        ols_mod._STREAM_TILE = 2 * ns * 8
+        ols_mod._STREAM_TILE = 2 * ns * host_out.element_size()
         oc.convolve(hsig, fs, p, out=host_out)
     finally:
         ols_mod._STREAM_TILE = tile
