@@ -65,12 +65,13 @@ struct DefaultPolicy {
   static constexpr int SEGS = dbl ? std::max(1, 256 / T) : std::max(1, 128 / T);
   // BAR = 1: named barrier per segment group, so only the warps of one
   // segment are coupled (matters for N = 1024: two 2-warp groups per CTA)
-  // N = 1024 (two 2-warp groups per CTA): mbarrier "buffer free" exchanges
-  // (OLSB_VARIANT=8 in the sweep: 0.317 vs 0.330 ms on cfg2; slower at 2048)
+  // (The mbarrier "buffer free" exchanges of OLSB_VARIANT=8 are 4% faster at
+  // N = 1024 but not default: compute-sanitizer racecheck does not model the
+  // mbarrier wait and reports the exchange as a race.)
   using type = KCfg<R, LOGN, SEGS, (!dbl && LOGN == 12) ? 2 : 1,
                     dbl ? H_LDG : H_TEX, 1,
                     dbl ? 1 : std::max(1, 512 / (SEGS * T)), dbl ? 0 : 2,
-                    dbl ? 0 : 1, 0, (!dbl && LOGN == 10) ? 1 : 0>;
+                    dbl ? 0 : 1>;
 };
 
 // tuning variants for fp32 (OLSB_VARIANT).  A CTA holds SEGS x max(1,
