@@ -394,3 +394,40 @@ def test_cfg5_geometry_windows_vs_oracle(oc):
         full[lo - (a - (m - 1)):] = xw
         ref = oracle.direct_window(full, taps, 0, m - 1, m - 1 + (b - a))
         assert rel_l2_per_filter(out.cpu().numpy(), ref) <= L2_TOL, a
+
+
+@pytest.mark.parametrize("mode", ["c2c", "r2r"])
+def test_beyond_int32_sample_indices_vs_oracle(oc, mode):
+    """N_s = 2^31 + 12345 samples (c2c: 17 GB in, 17 GB out): every sample
+    and output index crosses the int32 range.  Windows around 2^31, at the
+    end and at the start are compared with the oracle's direct float64
+    convolution; the full output is checked for coverage (no NaN left)."""
+    ns, m, nfil, n, origin = (1 << 31) + 12345, 64, 1, 1024, 5
+    real = mode == "r2r"
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    xs = torch.randn(ns, dtype=torch.float32 if real else torch.complex64,
+                     device="cuda", generator=gen)
+    rng = np.random.default_rng([3, m, nfil])
+    taps = rng.standard_normal((nfil, m)) + (
+        0 if real else 1j * rng.standard_normal((nfil, m)))
+    P = oc.Precision.single
+    p = oc.plan(ns, m, mode, origin, n)
+    fs = oc.transform_filters(oc.make_filterset(taps, origin, P), p,
+                              "natural" if real else "permuted")
+    sig = oc.Signal(samples=xs, length=ns, domain="time",
+                    value_kind="real" if real else "complex")
+    out = torch.full((nfil, ns), float("nan"), dtype=xs.dtype, device="cuda")
+    oc.convolve(sig, fs, p, out=out)
+    assert not torch.isnan(out).any()
+    for a in (0, (1 << 31) - 150, (1 << 31) + 7, ns - 300):
+        b = min(a + 300, ns)
+        # y[g] = sum_k h[k] x[g - k + origin]
+        lo, hi = a - (m - 1) + origin, b + origin
+        full = np.zeros(hi - lo, np.complex128)
+        clo, chi = max(lo, 0), min(hi, ns)
+        full[clo - lo:chi - lo] = xs[clo:chi].cpu().numpy()
+        ref = oracle.direct_window(full, taps, 0, m - 1, m - 1 + (b - a))
+        got = out[:, a:b].cpu().numpy()
+        assert rel_l2_per_filter(got, ref) <= L2_TOL, a
+    del out, xs
+    torch.cuda.empty_cache()
