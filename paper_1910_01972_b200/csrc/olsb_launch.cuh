@@ -62,7 +62,10 @@ struct DefaultPolicy {
   // 4 CTAs per SM, segment spectrum and runtime-window twiddles in TMEM, the
   // next filter's spectrum prefetched through the TEX path; N = 4096 double
   // buffers the exchange (one barrier per exchange).
-  static constexpr int SEGS = dbl ? std::max(1, 256 / T) : std::max(1, 128 / T);
+  // fp64: 128-thread CTAs (256 for N = 4096) at 3 CTAs/SM, 170 registers
+  // (OLSB_DVARIANT sweep: cfg3 shape 5.65 vs 6.12 ms for 256-thread CTAs at
+  // one CTA/SM)
+  static constexpr int SEGS = std::max(1, 128 / T);
   // BAR = 1: named barrier per segment group, so only the warps of one
   // segment are coupled (matters for N = 1024: two 2-warp groups per CTA)
   // (The mbarrier "buffer free" exchanges of OLSB_VARIANT=8 are 4% faster at
@@ -70,7 +73,9 @@ struct DefaultPolicy {
   // mbarrier wait and reports the exchange as a race.)
   using type = KCfg<R, LOGN, SEGS, (!dbl && LOGN == 12) ? 2 : 1,
                     dbl ? H_LDG : H_TEX, 1,
-                    dbl ? 1 : std::max(1, 512 / (SEGS * T)), dbl ? 0 : 2,
+                    dbl ? (SEGS * T >= 256 ? 1 : 3)
+                        : std::max(1, 512 / (SEGS * T)),
+                    dbl ? 0 : 2,
                     dbl ? 0 : 1>;
 };
 
@@ -149,9 +154,32 @@ int launch_fused_cfg(FusedArgs<typename C::R> a, cudaStream_t st) {
   return int(cudaGetLastError());
 }
 
+// fp64 tuning variants (OLSB_DVARIANT): 128-thread CTAs (one segment group
+// for N >= 2048) at 2 / 3 / 4 CTAs per SM (255 / 170 / 128 registers)
+inline int dvariant_env() {
+  static int v = [] {
+    const char* e = getenv("OLSB_DVARIANT");
+    return e ? atoi(e) : -1;
+  }();
+  return v;
+}
+template <int LOGN, int MINB>
+using DVariant = KCfg<double, LOGN, std::max(1, 128 / Geo<LOGN>::T), 1, H_LDG, 1,
+                      MINB>;
+
 template <class R, int LOGN>
 int launch_fused(FusedArgs<R> a, int mode, cudaStream_t st) {
   using D = typename DefaultPolicy<R, LOGN>::type;
+  if constexpr (std::is_same<R, double>::value) {
+    if (mode == FMODE_C2C) {
+      switch (dvariant_env()) {
+        case 2: return launch_fused_cfg<DVariant<LOGN, 2>>(a, st);
+        case 3: return launch_fused_cfg<DVariant<LOGN, 3>>(a, st);
+        case 4: return launch_fused_cfg<DVariant<LOGN, 4>>(a, st);
+        default: break;
+      }
+    }
+  }
   if (mode == FMODE_R2R) return launch_fused_cfg<D, FMODE_R2R>(a, st);
   if (mode == FMODE_ABS2) return launch_fused_cfg<D, FMODE_ABS2>(a, st);
   if constexpr (std::is_same<R, float>::value) {
