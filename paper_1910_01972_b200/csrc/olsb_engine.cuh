@@ -250,7 +250,7 @@ __device__ int g_twready;
 template <class R, int LOGN>
 __device__ __forceinline__ Tw<R> twiddle_value(int q_lo, int i, bool tan01) {
   int idx, l;
-  twiddle_decode(q_lo, i, &idx, &l);
+  twiddle_decode(q_lo, i, &idx, &l, std::is_same<R, double>::value);
   double c, t;
   twiddle_entry(q_lo, idx, l, tan01, &c, &t);
   return Tw<R>{R(c), R(t)};
@@ -490,11 +490,17 @@ __device__ __forceinline__ void st_cs_if(Cpx<double>* p, Cpx<double> v,
 // registers
 template <class R>
 struct TwSmem {
-  const Tw<R>* base;  // window table + 2 l
+  // window table + 2 l (fp32, [slot][l][half]) or + l (fp64, [slot][half][l],
+  // see twiddle_decode)
+  const Tw<R>* base;
   int lo;
+  static constexpr bool split = std::is_same<R, double>::value;
   __device__ __forceinline__ Tw<R> get0() const { return base[0]; }
   __device__ __forceinline__ TwPair<R> get2(int p) const {
-    return *reinterpret_cast<const TwPair<R>*>(base + (size_t(p) << (lo + 1)));
+    if constexpr (split)
+      return TwPair<R>{base[size_t(2 * p) << lo], base[size_t(2 * p + 1) << lo]};
+    else
+      return *reinterpret_cast<const TwPair<R>*>(base + (size_t(p) << (lo + 1)));
   }
 };
 template <class R>
@@ -509,7 +515,7 @@ struct TwRegs {
 template <class R, int LOGN, int Q>
 __device__ __forceinline__ TwSmem<R> tw_smem(const Tw<R>* tab, int t) {
   using G = Geo<LOGN>;
-  return TwSmem<R>{tab + 2 * G::low_bits(Q, t), G::lo(Q)};
+  return TwSmem<R>{tab + (TwSmem<R>::split ? 1 : 2) * G::low_bits(Q, t), G::lo(Q)};
 }
 template <int LOGN, int Q>
 __device__ __forceinline__ int top_bits(int t) {

@@ -739,11 +739,22 @@ OLSB_HD void twiddle_entry(int lo, int idx, int l, bool tan01, double* c,
 }
 
 // entry i of window lo's table -> (idx or -1, l)
-OLSB_HD void twiddle_decode(int lo, int i, int* idx, int* l) {
-  const int h = i & 1;
-  const int rest = i >> 1;
-  *l = rest & ((1 << lo) - 1);
-  const int sl = rest >> lo;
+// Table entry i of a window -> (idx, l).  fp32 tables are [slot][l][half]
+// (a thread's pair is one 16-byte load); fp64 tables are [slot][half][l]
+// (`split`: consecutive l are consecutive 16-byte entries, so a warp's
+// 128-bit loads are bank-conflict free).
+OLSB_HD void twiddle_decode(int lo, int i, int* idx, int* l, bool split = false) {
+  int h, sl;
+  if (split) {
+    *l = i & ((1 << lo) - 1);
+    h = (i >> lo) & 1;
+    sl = i >> (lo + 1);
+  } else {
+    h = i & 1;
+    const int rest = i >> 1;
+    *l = rest & ((1 << lo) - 1);
+    sl = rest >> lo;
+  }
   *idx = sl == 0 ? (h == 0 ? 0 : -1) : 2 * sl - 1 + h;
 }
 
