@@ -153,6 +153,41 @@ int olsb_fused_r2r_range(const void* x, int64_t x_base, int64_t n_s,
                          double pp_c, void* out, int64_t out_ld,
                          int64_t out_base, int precision, void* stream);
 
+/* Exact mode: the reference's arithmetic, bit for bit.  Same arguments as
+ * olsb_fused_c2c plus `tw`, the reference's twiddle table (n/2 complex
+ * values e^{-2 pi i j / n} rounded to the precision, fft.py:70-78; device
+ * memory), i.e. the `tw` argument of K.fused_c2c (_kernels_nb.py:266).  The
+ * engine then keeps the reference's segment grid (no 32-alignment), computes
+ * every butterfly as the reference's explicit complex product by the table
+ * entry (dif_fwd / dit_inv, _kernels_nb.py:11-51, twc = conj(tw)) with
+ * non-contracting IEEE operations, and applies 1/n and pp_c where dit_inv
+ * and _store do.  With spectra from olsb_filter_spectra_c2c_ref, outputs are
+ * bit-identical to the reference's fp32 (fp64) fused_c2c.  pp_kind: none or
+ * scale. */
+int olsb_fused_c2c_ref(const void* x, int64_t x_base, int64_t n_s,
+                       const void* spectra_dev, int n_fil, int n, int m,
+                       int origin, int64_t l_eff, int t0, int64_t win_off,
+                       int64_t seg_lo, int64_t seg_hi, int pp_kind,
+                       double pp_c, const void* tw, void* out, int64_t out_ld,
+                       int64_t out_base, int precision, void* stream);
+
+/* Exact-mode |y|^2 epilogue: replaces K.fused_c2c_abs2(x, spectra, tw, twc,
+ * ...) (_kernels_nb.py:288-309) bit for bit. */
+int olsb_fused_c2c_abs2_ref(const void* x, int64_t x_base, int64_t n_s,
+                            const void* spectra_dev, int n_fil, int n, int m,
+                            int origin, int64_t l_eff, int t0, int64_t win_off,
+                            int64_t seg_lo, int64_t seg_hi, const void* tw,
+                            void* out, int64_t out_ld, int64_t out_base,
+                            int precision, void* stream);
+
+/* Exact-mode filter spectra: the pad + K.dif_fwd_batch(mat, tw) of
+ * transform_filters (ols.py:195-199, _kernels_nb.py:54-57) with the
+ * reference's arithmetic; same outputs as olsb_filter_spectra_c2c. */
+int olsb_filter_spectra_c2c_ref(const void* taps, int n_fil, int m, int n,
+                                const void* tw, void* spectra_perm,
+                                void* spectra_dev, int precision,
+                                void* stream);
+
 /* Input samples [*x_lo, *x_hi) that olsb_fused_c2c_range(g_lo, g_hi) reads
  * (before clipping to [0, n_s)): the shard plus its halos. */
 int olsb_input_extent(int n, int m, int origin, int64_t g_lo, int64_t g_hi,

@@ -37,6 +37,16 @@ SIGNATURES = {
     "olsb_fused_c2c_range": (c_int, [c_vp, c_i64, c_i64, c_vp, c_int, c_int,
                                      c_int, c_int, c_i64, c_i64, c_int, c_dbl,
                                      c_vp, c_i64, c_i64, c_int, c_vp]),
+    "olsb_fused_c2c_ref": (c_int, [c_vp, c_i64, c_i64, c_vp, c_int, c_int,
+                                   c_int, c_int, c_i64, c_int, c_i64, c_i64,
+                                   c_i64, c_int, c_dbl, c_vp, c_vp, c_i64,
+                                   c_i64, c_int, c_vp]),
+    "olsb_fused_c2c_abs2_ref": (c_int, [c_vp, c_i64, c_i64, c_vp, c_int,
+                                        c_int, c_int, c_int, c_i64, c_int,
+                                        c_i64, c_i64, c_i64, c_vp, c_vp,
+                                        c_i64, c_i64, c_int, c_vp]),
+    "olsb_filter_spectra_c2c_ref": (c_int, [c_vp, c_int, c_int, c_int, c_vp,
+                                            c_vp, c_vp, c_int, c_vp]),
     "olsb_fused_c2c_abs2": (c_int, [c_vp, c_i64, c_i64, c_vp, c_int, c_int,
                                     c_int, c_int, c_i64, c_int, c_i64, c_i64,
                                     c_i64, c_vp, c_i64, c_i64, c_int, c_vp]),

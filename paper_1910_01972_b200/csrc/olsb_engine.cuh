@@ -107,7 +107,10 @@ struct KCfg {
       P >= 2 ? al(NBUF * buf_elems * sizeof(Cpx<R>)) : 0;
   // ---- row kernels: every twiddle table in shared memory, then buffers
   static constexpr size_t tab_bytes = al(size_t(G::tw_total()) * sizeof(Tw<R>));
-  static constexpr size_t smem_bytes = tab_bytes + bufs_bytes;
+  // exact mode: junction-window table (15 broadcast entries) at the end
+  static constexpr size_t jt_bytes = al(16 * sizeof(Tw<R>));
+  static constexpr size_t jt_off = tab_bytes + bufs_bytes;
+  static constexpr size_t smem_bytes = jt_off + jt_bytes;
   // ---- fused kernel: [bufs (+ top table at init) | low tables | TMEM slot]
   static constexpr int lowtab_elems = TOPOUT ? G::tw_offset(P - 1) : G::tw_total();
   static constexpr size_t f_bufs_bytes =
@@ -120,7 +123,8 @@ struct KCfg {
   static constexpr size_t f_slot_off = f_tab_off + f_tab_bytes;
   // [TMEM base address slot | MB: one mbarrier per segment group]
   static constexpr size_t f_mbar_off = f_slot_off + 16;
-  static constexpr size_t f_smem_bytes = f_mbar_off + (MB ? 8 * SEGS : 0);
+  static constexpr size_t f_jt_off = al(f_mbar_off + (MB ? 8 * SEGS : 0));
+  static constexpr size_t f_smem_bytes = f_jt_off + jt_bytes;
 };
 
 // configuration of the row kernels (filter spectra, standalone transforms)
@@ -274,9 +278,43 @@ __global__ void tw_table_kernel() {
 // Window q's table goes to lowtab + tw_offset(q), except the top window's
 // when `toptab` is given.  Copied from the device-wide table once it is
 // ready, else computed here (same values bit for bit).
+// exact mode: entry (idx = 2^j - 1 + k, l) of window lo is the caller's
+// fp32 / fp64 table value tw[(l + k 2^lo) * (N >> (lo + j + 1))]
 template <class R, int LOGN>
-__device__ void build_tables(Tw<R>* lowtab, Tw<R>* toptab) {
+__device__ __forceinline__ Tw<R> ref_entry(const Cpx<R>* xtw, int lo, int idx,
+                                           int l) {
+  if (idx < 0) return Tw<R>{R(0), R(0)};
+  int j = 0;
+  while ((2 << j) - 1 <= idx) ++j;
+  const int k = idx - ((1 << j) - 1);
+  const Cpx<R> w = xtw[(l + (k << lo)) * ((1 << LOGN) >> (lo + j + 1))];
+  return Tw<R>{w.re, w.im};
+}
+// exact mode: junction-window entries jt[2^j - 1 + k] = tw[k * (N >> (j + 1))]
+template <class R, int LOGN>
+__device__ void build_jt(Tw<R>* jt, const Cpx<R>* xtw) {
+  constexpr int G0 = Geo<LOGN>::G0;
+  for (int i = threadIdx.x; i < (1 << G0) - 1; i += blockDim.x)
+    jt[i] = ref_entry<R, LOGN>(xtw, 0, i, 0);
+}
+
+template <class R, int LOGN>
+__device__ void build_tables(Tw<R>* lowtab, Tw<R>* toptab,
+                             const Cpx<R>* xtw = nullptr) {
   using G = Geo<LOGN>;
+  if (xtw) {
+    sfor<1, G::P>([&](auto qc) {
+      constexpr int q = decltype(qc)::value;
+      constexpr int lo = G::lo(q);
+      Tw<R>* dst = (q == G::P - 1 && toptab) ? toptab : lowtab + G::tw_offset(q);
+      for (int i = threadIdx.x; i < G::tw_entries(q); i += blockDim.x) {
+        int idx, l;
+        twiddle_decode(lo, i, &idx, &l, std::is_same<R, double>::value);
+        dst[i] = ref_entry<R, LOGN>(xtw, lo, idx, l);
+      }
+    });
+    return;
+  }
   int ready;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];"
                : "=r"(ready)
@@ -562,31 +600,41 @@ __device__ __forceinline__ void exchange(Cpx<typename C::R>* bufs, int& xc,
 // full forward transform: x holds window P-1 on entry, window 0 (J) on exit.
 // With TOPREG the top window's 15 twiddles come from `twr`; with TMX the
 // runtime windows' twiddles are read from TMEM at `tb`.
-template <class C, bool TOPREG>
+template <class C, bool TOPREG, bool XR = false>
 __device__ __forceinline__ void forward_fft(Cpx<typename C::R>* x,
                                             const Tw<typename C::R>* lowtab,
                                             const Tw<typename C::R>* twr,
                                             Cpx<typename C::R>* bufs, int& xc,
-                                            int sl, int t, uint32_t tb = 0) {
+                                            int sl, int t, uint32_t tb = 0,
+                                            const Tw<typename C::R>* jt = nullptr) {
   using R = typename C::R;
   using G = typename C::G;
   constexpr int LOGN = C::LOGN;
   sfor<0, G::P>([&](auto qr) {
     constexpr int q = G::P - 1 - decltype(qr)::value;
     if constexpr (q < G::P - 1) exchange<C, q + 1, q>(bufs, xc, sl, t, x);
+    auto pass = [&](const auto& tws) {
+      if constexpr (XR) {
+        pass_ref<R, false>(x, tws);
+      } else {
+        dif_pass_rt<R, G::tan01(q)>(x, tws, top_bits<LOGN, q>(t));
+      }
+    };
     if constexpr (q == 0) {
-      dif_pass_static<R, C::LOGE, G::G0>(x);
+      if constexpr (XR) {
+        pass_static_ref<R, C::LOGE, G::G0, false>(x, jt);
+      } else {
+        dif_pass_static<R, C::LOGE, G::G0>(x);
+      }
     } else {
       if constexpr (C::TMX && (q == G::P - 1 || (q == G::P - 2 && C::TMX == 2))) {
         Tw<R> tw[16];
         tmem_ld_tw(tb + (q == G::P - 1 ? 32u : 64u), tw);
-        dif_pass_rt<R, G::tan01(q)>(x, TwRegs<R>{tw}, top_bits<LOGN, q>(t));
+        pass(TwRegs<R>{tw});
       } else if constexpr (q == G::P - 1 && TOPREG) {
-        dif_pass_rt<R, G::tan01(q)>(x, TwRegs<R>{twr}, top_bits<LOGN, q>(t));
+        pass(TwRegs<R>{twr});
       } else {
-        dif_pass_rt<R, G::tan01(q)>(
-            x, tw_smem<R, LOGN, q>(lowtab + G::tw_offset(q), t),
-            top_bits<LOGN, q>(t));
+        pass(tw_smem<R, LOGN, q>(lowtab + G::tw_offset(q), t));
       }
     }
   });
@@ -616,6 +664,9 @@ struct FusedArgs {
   // real |y|^2 output)
   const R* xr;
   R* outr;
+  // exact mode: the reference's twiddle table tw[j] = e^{-2 pi i j / N},
+  // j < N/2, rounded to R (fft.py:70-78); null for the fast path
+  const Cpx<R>* xtw;
 };
 
 // fused-kernel data modes
@@ -646,7 +697,9 @@ __device__ __forceinline__ void st_cs_mask_r(double* p, double v, unsigned mask)
       : "memory");
 }
 
-template <class C, int MODE = FMODE_C2C>
+// XR: exact mode (reference arithmetic, bit-identical to the reference's
+// kernels; C2C and ABS2 only)
+template <class C, int MODE = FMODE_C2C, bool XR = false>
 __global__ void __launch_bounds__(C::THREADS, C::MINB)
     fused_c2c_kernel(const FusedArgs<typename C::R> a) {
   using R = typename C::R;
@@ -672,8 +725,11 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     if (tid < 32) tmem_alloc<C::TCOLS>(tslot);
     tmem_fence_before();
   }
+  Tw<R>* jt = reinterpret_cast<Tw<R>*>(smem_raw + C::f_jt_off);
   build_tables<R, LOGN>(lowtab,
-                        C::TOPOUT ? reinterpret_cast<Tw<R>*>(bufs) : nullptr);
+                        C::TOPOUT ? reinterpret_cast<Tw<R>*>(bufs) : nullptr,
+                        XR ? a.xtw : nullptr);
+  if constexpr (XR) build_jt<R, LOGN>(jt, a.xtw);
   if constexpr (C::MB) {
     if (tid < C::SEGS) mbar_init(group_mbar<C>(tid), T / 32);
   }
@@ -840,8 +896,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     // ---- forward FFT (dif_fwd, _kernels_nb.py:11-28); the spectrum stays in
     // registers (or TMEM) with the inverse's 1/N and the scale post-process
     // folded in
-    forward_fft<C, C::TOPREG>(x, lowtab, twr, bufs, xc, sl, t, tb);
-    {
+    forward_fft<C, C::TOPREG, XR>(x, lowtab, twr, bufs, xc, sl, t, tb, jt);
+    if constexpr (!XR) {
       const R sc = a.pp_kind == OLSB_PP_SCALE ? inv_n * a.pp_c : inv_n;
 #pragma unroll
       for (int e = 0; e < E; ++e) x[e] = cscale(x[e], sc);
@@ -858,9 +914,16 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
       Cpx<R> y[E];
       if constexpr (C::TMX) tmem_ld_cpx(tb, y);  // y = segment spectrum
       const Cpx<R>* xs = C::TMX ? y : x;
+      auto mul1 = [&](Cpx<R> xv, Cpx<R> hv) {
+        if constexpr (XR) {
+          return cmul_ref(xv, hv);
+        } else {
+          return cmul(xv, hv);
+        }
+      };
       auto mulh = [&](int u, float4 h) {
-        y[2 * u] = cmul(xs[2 * u], Cpx<R>{R(h.x), R(h.y)});
-        y[2 * u + 1] = cmul(xs[2 * u + 1], Cpx<R>{R(h.z), R(h.w)});
+        y[2 * u] = mul1(xs[2 * u], Cpx<R>{R(h.x), R(h.y)});
+        y[2 * u + 1] = mul1(xs[2 * u + 1], Cpx<R>{R(h.z), R(h.w)});
       };
       if constexpr (C::PREF) {
         sfor<0, C::VPT>([&](auto uc) {
@@ -882,27 +945,46 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
           if constexpr (V16<R>::per == 2) {
             mulh(u, h);
           } else {
-            y[u] = cmul(x[u], Cpx<R>{h.x, h.y});
+            y[u] = mul1(x[u], Cpx<R>{h.x, h.y});
           }
         });
       }
       // ---- inverse FFT (dit_inv, _kernels_nb.py:31-51)
-      dit_pass_static<R, C::LOGE, G::G0>(y);
+      if constexpr (XR) {
+        pass_static_ref<R, C::LOGE, G::G0, true>(y, jt);
+      } else {
+        dit_pass_static<R, C::LOGE, G::G0>(y);
+      }
       sfor<1, P>([&](auto qc) {
         constexpr int q = decltype(qc)::value;
         exchange<C, q - 1, q>(bufs, xc, sl, t, y, IC<C::ABL>{});
+        auto pass = [&](const auto& tws) {
+          if constexpr (XR) {
+            pass_ref<R, true>(y, tws);
+          } else {
+            dit_pass_rt<R, G::tan01(q)>(y, tws, top_bits<LOGN, q>(t));
+          }
+        };
         if constexpr (C::TMX && (q == P - 1 || (q == P - 2 && C::TMX == 2))) {
           Tw<R> tw[16];
           tmem_ld_tw(tb + (q == P - 1 ? 32u : 64u), tw);
-          dit_pass_rt<R, G::tan01(q)>(y, TwRegs<R>{tw}, top_bits<LOGN, q>(t));
+          pass(TwRegs<R>{tw});
         } else if constexpr (q == P - 1 && C::TOPREG) {
-          dit_pass_rt<R, G::tan01(q)>(y, TwRegs<R>{twr}, top_bits<LOGN, q>(t));
+          pass(TwRegs<R>{twr});
         } else {
-          dit_pass_rt<R, G::tan01(q)>(
-              y, tw_smem<R, LOGN, q>(lowtab + G::tw_offset(q), t),
-              top_bits<LOGN, q>(t));
+          pass(tw_smem<R, LOGN, q>(lowtab + G::tw_offset(q), t));
         }
       });
+      if constexpr (XR) {
+        // dit_inv's final 1/N (exact: a power of two), then _store's pp_c
+        const bool scl = a.pp_kind == OLSB_PP_SCALE;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          Cpx<R> v{mul_rn(y[e].re, inv_n), mul_rn(y[e].im, inv_n)};
+          if (scl) v = Cpx<R>{mul_rn(a.pp_c, v.re), mul_rn(a.pp_c, v.im)};
+          y[e] = v;
+        }
+      }
       // ---- valid-sample writeback (_store kind 0/1, _kernels_nb.py:218-222):
       // in-place sample p is output o = p - t0 of this segment, kept iff
       // o_lo <= o < o_hi.  With the 32-aligned engine grid every warp store
@@ -971,7 +1053,11 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
         sfor<0, E>([&](auto ec) {
           constexpr int e = decltype(ec)::value;
           constexpr int pe = G::elem_part(P - 1, e);
-          if constexpr (MODE == FMODE_ABS2) {
+          if constexpr (MODE == FMODE_ABS2 && XR) {
+            st_cs_mask_r<(1u << e)>(
+                orow + pe,
+                add_rn(mul_rn(y[e].re, y[e].re), mul_rn(y[e].im, y[e].im)), vmask);
+          } else if constexpr (MODE == FMODE_ABS2) {
             st_cs_mask_r<(1u << e)>(orow + pe,
                                     fmaR(y[e].re, y[e].re, y[e].im * y[e].im),
                                     vmask);
@@ -1003,9 +1089,10 @@ struct RowsArgs {
   int rows;
   Cpx<R>* out_perm;                // may be null
   typename V16<R>::type* out_dev;  // may be null
+  const Cpx<R>* xtw;               // exact mode: the reference's tw table
 };
 
-template <class C>
+template <class C, bool XR = false>
 __global__ void __launch_bounds__(C::THREADS)
     fwd_rows_kernel(const RowsArgs<typename C::R> a) {
   using R = typename C::R;
@@ -1014,8 +1101,10 @@ __global__ void __launch_bounds__(C::THREADS)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Tw<R>* tab = reinterpret_cast<Tw<R>*>(smem_raw);
   Cpx<R>* bufs = reinterpret_cast<Cpx<R>*>(smem_raw + C::tab_bytes);
+  Tw<R>* jt = reinterpret_cast<Tw<R>*>(smem_raw + C::jt_off);
   const int sl = threadIdx.x / T, t = threadIdx.x % T;
-  build_tables<R, C::LOGN>(tab, nullptr);
+  build_tables<R, C::LOGN>(tab, nullptr, XR ? a.xtw : nullptr);
+  if constexpr (XR) build_jt<R, C::LOGN>(jt, a.xtw);
   __syncthreads();
   int xc = 0;
   const int ngroups = (a.rows + C::SEGS - 1) / C::SEGS;
@@ -1035,7 +1124,7 @@ __global__ void __launch_bounds__(C::THREADS)
     }
     // every load of the group precedes any store (in-place safety)
     __syncthreads();
-    forward_fft<C, false>(x, tab, nullptr, bufs, xc, sl, t);
+    forward_fft<C, false, XR>(x, tab, nullptr, bufs, xc, sl, t, 0, jt);
     if (live) {
       if (a.out_perm) {
         Cpx<R>* o = a.out_perm + size_t(r) * G::N + G::thread_part(0, t);

@@ -689,6 +689,106 @@ OLSB_HD void dif_pass_rt(Cpx<R>* x, const TW& tw, int hb) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Reference-arithmetic passes (exact mode).  The same stage / element pairing
+// as the fast passes (the reference's in-place radix-2 positions), but every
+// butterfly is the reference's: an explicit complex product by the fp32
+// table entry w = tw[(p mod 2^b) * (N >> (b + 1))] (dif_fwd, dit_inv with
+// twc = conj(tw), _kernels_nb.py:11-51), written with non-contracting
+// round-to-nearest intrinsics so no FMA is formed.  Tw fields hold (re, im)
+// of w here.  Results are bit-identical to the reference's fp32 (and fp64)
+// kernels.
+// ---------------------------------------------------------------------------
+#if defined(__CUDACC__)
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+
+// a * b as the reference computes complex products (oracle cmul)
+template <class R>
+__device__ __forceinline__ Cpx<R> cmul_ref(Cpx<R> a, Cpx<R> b) {
+  return Cpx<R>{sub_rn(mul_rn(a.re, b.re), mul_rn(a.im, b.im)),
+                add_rn(mul_rn(a.re, b.im), mul_rn(a.im, b.re))};
+}
+// dit_inv butterfly: v' = v * conj(w); u, v <- u + v', u - v'
+template <class R>
+__device__ __forceinline__ void dit_ref(Cpx<R>& u, Cpx<R>& v, Tw<R> w) {
+  const Cpx<R> p = cmul_ref(v, Cpx<R>{w.c, -w.t});
+  const Cpx<R> a{add_rn(u.re, p.re), add_rn(u.im, p.im)};
+  v = Cpx<R>{sub_rn(u.re, p.re), sub_rn(u.im, p.im)};
+  u = a;
+}
+// dif_fwd butterfly: u, v <- u + v, (u - v) * w
+template <class R>
+__device__ __forceinline__ void dif_ref(Cpx<R>& u, Cpx<R>& v, Tw<R> w) {
+  const Cpx<R> d{sub_rn(u.re, v.re), sub_rn(u.im, v.im)};
+  u = Cpx<R>{add_rn(u.re, v.re), add_rn(u.im, v.im)};
+  v = cmul_ref(d, Cpx<R>{w.c, w.t});
+}
+
+// runtime window (4 stages over 16 elements), entries idx = 2^j - 1 + k
+template <class R, bool INV, class TW>
+__device__ __forceinline__ void pass_ref(Cpx<R>* x, const TW& tw) {
+  auto stage = [&](auto jc) {
+    constexpr int j = decltype(jc)::value;
+    auto bf = [&](Tw<R> w, auto kc) {
+      constexpr int k = decltype(kc)::value;
+      sfor<0, (8 >> j)>([&](auto hc) {
+        constexpr int a = (decltype(hc)::value << (j + 1)) | k;
+        if constexpr (INV) {
+          dit_ref(x[a], x[a | (1 << j)], w);
+        } else {
+          dif_ref(x[a], x[a | (1 << j)], w);
+        }
+      });
+    };
+    if constexpr (j == 0) {
+      bf(tw.get0(), IC<0>{});
+    } else {
+      sfor<(1 << (j - 1)), (1 << j)>([&](auto pc) {
+        constexpr int pp = decltype(pc)::value;
+        const TwPair<R> w = tw.get2(pp);
+        bf(w.a, IC<2 * pp - 1 - ((1 << j) - 1)>{});
+        bf(w.b, IC<2 * pp - ((1 << j) - 1)>{});
+      });
+    }
+  };
+  if constexpr (INV) {
+    sfor<0, 4>([&](auto jc) { stage(jc); });
+  } else {
+    sfor<0, 4>([&](auto jr) { stage(IC<3 - decltype(jr)::value>{}); });
+  }
+}
+
+// junction window (lo = 0): G stages, entries jt[2^j - 1 + k] (broadcast)
+template <class R, int LOGE, int G, bool INV>
+__device__ __forceinline__ void pass_static_ref(Cpx<R>* x, const Tw<R>* jt) {
+  constexpr int E = 1 << LOGE;
+  auto stage = [&](auto jc) {
+    constexpr int j = decltype(jc)::value;
+    sfor<0, E / 2>([&](auto bc) {
+      constexpr int b = decltype(bc)::value;
+      constexpr int a = ((b >> j) << (j + 1)) | (b & ((1 << j) - 1));
+      constexpr int k = a & ((1 << j) - 1);
+      const Tw<R> w = jt[(1 << j) - 1 + k];
+      if constexpr (INV) {
+        dit_ref(x[a], x[a | (1 << j)], w);
+      } else {
+        dif_ref(x[a], x[a | (1 << j)], w);
+      }
+    });
+  };
+  if constexpr (INV) {
+    sfor<0, G>([&](auto jc) { stage(jc); });
+  } else {
+    sfor<0, G>([&](auto jr) { stage(IC<G - 1 - decltype(jr)::value>{}); });
+  }
+}
+#endif
+
 // Table slot of twiddle idx: slot s = (idx + 1) / 2 holds the pair
 // (2s - 1, 2s) (slot 0: idx 0 and an unused half); half = 1 for even idx > 0.
 OLSB_HD constexpr int twiddle_slot(int idx) { return (idx + 1) >> 1; }

@@ -229,6 +229,28 @@ int olsb_filter_spectra_c2c(const void* taps, int n_fil, int m, int n,
   });
 }
 
+int olsb_filter_spectra_c2c_ref(const void* taps, int n_fil, int m, int n,
+                                const void* tw, void* spectra_perm,
+                                void* spectra_dev, int precision,
+                                void* stream) {
+  const int logn = log2_of(n);
+  if (logn < 0) return OLSB_E_BAD_LENGTH;
+  if (n_fil < 0 || m < 1 || m > n || (n_fil > 0 && !taps) || !tw)
+    return OLSB_E_BAD_ARG;
+  if (n_fil == 0 || (!spectra_perm && !spectra_dev)) return 0;
+  return dispatch_prec(precision, [&](auto rv) {
+    using R = decltype(rv);
+    return dispatch_n<R>(logn, [&](auto lc) {
+      RowsArgs<R> a{static_cast<const Cpx<R>*>(taps), m, m, n_fil,
+                    static_cast<Cpx<R>*>(spectra_perm),
+                    static_cast<typename V16<R>::type*>(spectra_dev),
+                    static_cast<const Cpx<R>*>(tw)};
+      return launch_fwd_rows<R, decltype(lc)::value>(
+          a, static_cast<cudaStream_t>(stream));
+    });
+  });
+}
+
 int olsb_spectra_perm_to_dev(const void* spectra_perm, int n_fil, int n,
                              void* spectra_dev, int precision, void* stream) {
   const int logn = log2_of(n);
@@ -269,26 +291,33 @@ static int fused_range(int mode, const void* x, int64_t x_base, int64_t n_s,
                        const void* spectra_dev, int n_fil, int n, int t0,
                        int origin, int64_t l_eff, int64_t g_lo, int64_t g_hi,
                        int pp_kind, double pp_c, void* out, int64_t out_ld,
-                       int64_t out_base, int precision, void* stream) {
+                       int64_t out_base, int precision, void* stream,
+                       const void* xtw = nullptr) {
   const int logn = log2_of(n);
   if (logn < 0) return OLSB_E_BAD_LENGTH;
-  const bool pp_ok = pp_kind == OLSB_PP_NONE || pp_kind == OLSB_PP_SCALE ||
-                     (mode == FMODE_R2R && pp_kind == OLSB_PP_MAG2) ||
-                     (mode != FMODE_ABS2 && pp_kind == OLSB_PP_DERIV &&
-                      t0 >= 1 && t0 + l_eff <= n - 1);
+  const bool pp_ok =
+      xtw ? (mode == FMODE_C2C && (pp_kind == OLSB_PP_NONE ||
+                                   pp_kind == OLSB_PP_SCALE)) ||
+                (mode == FMODE_ABS2 && pp_kind == OLSB_PP_NONE)
+          : pp_kind == OLSB_PP_NONE || pp_kind == OLSB_PP_SCALE ||
+                (mode == FMODE_R2R && pp_kind == OLSB_PP_MAG2) ||
+                (mode != FMODE_ABS2 && pp_kind == OLSB_PP_DERIV && t0 >= 1 &&
+                 t0 + l_eff <= n - 1);
   if (!pp_ok) return OLSB_E_UNSUPPORTED;
   if (n_s < 1 || n_fil < 0 || g_lo < 0 || g_hi < g_lo) return OLSB_E_BAD_ARG;
   if (l_eff < 1 || t0 < 0 || t0 + l_eff > n) return OLSB_E_GEOMETRY;
   if (g_hi > n_s) g_hi = n_s;
   if (n_fil == 0 || g_hi <= g_lo) return 0;
   if (!x || !spectra_dev || !out) return OLSB_E_BAD_ARG;
-  int t0e;
-  long long le;
-  engine_grid(n, t0, l_eff, &t0e, &le);
+  int t0e = t0;
+  long long le = l_eff;
+  // exact mode keeps the reference's segment grid
+  if (!xtw) engine_grid(n, t0, l_eff, &t0e, &le);
   return dispatch_prec(precision, [&](auto rv) {
     using R = decltype(rv);
     return dispatch_n<R>(logn, [&](auto lc) {
       FusedArgs<R> a = {};
+      a.xtw = static_cast<const Cpx<R>*>(xtw);
       a.x = static_cast<const Cpx<R>*>(x);
       a.xr = static_cast<const R*>(x);
       a.x_base = x_base;
@@ -346,6 +375,38 @@ int olsb_fused_c2c(const void* x, int64_t x_base, int64_t n_s,
                      origin, l_eff, seg_lo * l_eff,
                      std::min<int64_t>(seg_hi * l_eff, n_s), pp_kind, pp_c,
                      out, out_ld, out_base, precision, stream);
+}
+
+int olsb_fused_c2c_ref(const void* x, int64_t x_base, int64_t n_s,
+                       const void* spectra_dev, int n_fil, int n, int m,
+                       int origin, int64_t l_eff, int t0, int64_t win_off,
+                       int64_t seg_lo, int64_t seg_hi, int pp_kind,
+                       double pp_c, const void* tw, void* out, int64_t out_ld,
+                       int64_t out_base, int precision, void* stream) {
+  const int rc = check_ref_geometry(n_s, n_fil, n, m, origin, l_eff, t0,
+                                    win_off, seg_lo, seg_hi);
+  if (rc) return rc;
+  if (!tw) return OLSB_E_BAD_ARG;
+  return fused_range(FMODE_C2C, x, x_base, n_s, spectra_dev, n_fil, n, t0,
+                     origin, l_eff, seg_lo * l_eff,
+                     std::min<int64_t>(seg_hi * l_eff, n_s), pp_kind, pp_c,
+                     out, out_ld, out_base, precision, stream, tw);
+}
+
+int olsb_fused_c2c_abs2_ref(const void* x, int64_t x_base, int64_t n_s,
+                            const void* spectra_dev, int n_fil, int n, int m,
+                            int origin, int64_t l_eff, int t0, int64_t win_off,
+                            int64_t seg_lo, int64_t seg_hi, const void* tw,
+                            void* out, int64_t out_ld, int64_t out_base,
+                            int precision, void* stream) {
+  const int rc = check_ref_geometry(n_s, n_fil, n, m, origin, l_eff, t0,
+                                    win_off, seg_lo, seg_hi);
+  if (rc) return rc;
+  if (!tw) return OLSB_E_BAD_ARG;
+  return fused_range(FMODE_ABS2, x, x_base, n_s, spectra_dev, n_fil, n, t0,
+                     origin, l_eff, seg_lo * l_eff,
+                     std::min<int64_t>(seg_hi * l_eff, n_s), OLSB_PP_NONE, 1.0,
+                     out, out_ld, out_base, precision, stream, tw);
 }
 
 int olsb_fused_c2c_abs2(const void* x, int64_t x_base, int64_t n_s,

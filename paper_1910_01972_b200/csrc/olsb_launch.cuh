@@ -129,10 +129,10 @@ int ensure_twiddle_table(cudaStream_t st) {
   return int(cudaGetLastError());
 }
 
-template <class C, int MODE = FMODE_C2C>
+template <class C, int MODE = FMODE_C2C, bool XR = false>
 int launch_fused_cfg(FusedArgs<typename C::R> a, cudaStream_t st) {
   if (int rc = ensure_twiddle_table<typename C::R, C::LOGN>(st)) return rc;
-  auto kern = fused_c2c_kernel<C, MODE>;
+  auto kern = fused_c2c_kernel<C, MODE, XR>;
   int resident = 0;
   int rc = prepare(kern, C::f_smem_bytes, C::THREADS, &resident);
   if (rc) return rc;
@@ -170,6 +170,11 @@ using DVariant = KCfg<double, LOGN, std::max(1, 128 / Geo<LOGN>::T), 1, H_LDG, 1
 template <class R, int LOGN>
 int launch_fused(FusedArgs<R> a, int mode, cudaStream_t st) {
   using D = typename DefaultPolicy<R, LOGN>::type;
+  if (a.xtw) {  // exact mode (reference arithmetic), default policy
+    if (mode == FMODE_ABS2) return launch_fused_cfg<D, FMODE_ABS2, true>(a, st);
+    if (mode == FMODE_C2C) return launch_fused_cfg<D, FMODE_C2C, true>(a, st);
+    return OLSB_E_UNSUPPORTED;
+  }
   if constexpr (std::is_same<R, double>::value) {
     if (mode == FMODE_C2C) {
       switch (dvariant_env()) {
@@ -202,7 +207,7 @@ int launch_fused(FusedArgs<R> a, int mode, cudaStream_t st) {
 template <class R, int LOGN>
 int launch_fwd_rows(RowsArgs<R> a, cudaStream_t st) {
   using C = RowCfg<R, LOGN>;
-  auto kern = fwd_rows_kernel<C>;
+  auto kern = a.xtw ? fwd_rows_kernel<C, true> : fwd_rows_kernel<C, false>;
   int resident = 0;
   int rc = prepare(kern, C::smem_bytes, C::THREADS, &resident);
   if (rc) return rc;

@@ -39,7 +39,8 @@ from .fft import DEFAULT_MAX_FFT_LEN
 from .postproc import NONE, PostProcSpec
 
 MODES = ("c2c", "r2r")
-ENGINE_VARIANTS = ("fused", "pipelined", "full_fft_baseline", "direct_oracle")
+ENGINE_VARIANTS = ("fused", "pipelined", "full_fft_baseline", "direct_oracle",
+                   "fused_exact")
 
 DEFAULT_MAX_FULL_LEN = 1 << 25
 PIPELINED_DEFAULT_SEGMENT = 8192
@@ -150,7 +151,8 @@ def _chunk_bounds(n_items: int, workers: int) -> List[Tuple[int, int]]:
 
 
 def _required_layout(mode: str, variant: str) -> str:
-    return "permuted" if (mode == "c2c" and variant == "fused") else "natural"
+    return ("permuted" if (mode == "c2c" and variant in ("fused", "fused_exact"))
+            else "natural")
 
 
 def _stream_ptr() -> int:
@@ -289,6 +291,11 @@ def convolve(signal: Signal, filters: FilterSet, seg_plan: SegmentPlan,
     _check_inputs(signal, filters, seg_plan)
     precision = signal.precision
 
+    if variant == "fused_exact" and (seg_plan.mode != "c2c" or pp.kind not in (
+            "none", "scale", "magnitude_squared")):
+        raise EngineError("variant 'fused_exact' (the reference's arithmetic) "
+                          "covers c2c with postproc none | scale | "
+                          "magnitude_squared")
     if pp.kind == "derivative" and (seg_plan.tap_len == 1
                                     or variant != "fused"):
         # M = 1 has no halo (the reference recomputes seam neighbours from the
@@ -357,8 +364,61 @@ def convolve(signal: Signal, filters: FilterSet, seg_plan: SegmentPlan,
                              l_eff, t0, win_off, lo, hi, pp, out, n_s, 0,
                              precision)
         return out
+    if variant == "fused_exact":
+        return _fused_exact(signal, filters, seg_plan, pp, precision, l_eff,
+                            t0, win_off, n_seg_eff, out, out_dtype, workers)
     return _pipelined(signal, filters, seg_plan, pp, precision, l_eff, t0,
                       win_off, n_seg_eff, out)
+
+
+_REF_TW = {}
+
+
+def _ref_twiddles(n: int, precision: Precision, device) -> torch.Tensor:
+    """The reference's twiddle table tw[j] = e^{-2 pi i j / n}, j < n/2, as
+    fft.py:70-78 builds it (numpy, rounded to the precision), on `device`."""
+    key = (n, precision, str(device))
+    t = _REF_TW.get(key)
+    if t is None:
+        from .fft import _tables
+        tw = _tables(n, n // 2, precision)[0]
+        t = torch.from_numpy(np.array(tw)).to(device)
+        _REF_TW[key] = t
+    return t
+
+
+def _fused_exact(signal, filters, seg_plan, pp, precision, l_eff, t0,
+                 win_off, n_seg, out, out_dtype, workers):
+    """variant="fused_exact": the fused engine with the reference's
+    arithmetic (olsb_fused_c2c_ref): outputs bit-identical to the
+    reference's fp32 / fp64 ``convolve(variant="fused")``."""
+    if not signal.samples.is_cuda or (out is not None and not out.is_cuda):
+        raise ValueError("variant 'fused_exact' runs on device-resident "
+                         "signal and output")
+    n, n_s, n_fil = seg_plan.fft_len, signal.length, filters.n_filters
+    dev = signal.samples.device
+    tw = _ref_twiddles(n, precision, dev)
+    taps = filters.taps.to(device=dev, dtype=precision.torch_complex)
+    taps = taps.contiguous()
+    spec = torch.empty((n_fil, n), dtype=precision.torch_complex, device=dev)
+    if out is None:
+        out = torch.empty((n_fil, n_s), dtype=out_dtype, device=dev)
+    with torch.cuda.device(dev):
+        _lib.call("olsb_filter_spectra_c2c_ref", taps.data_ptr(), n_fil,
+                  seg_plan.tap_len, n, tw.data_ptr(), None, spec.data_ptr(),
+                  precision.code, _stream_ptr())
+        for lo, hi in _chunk_bounds(n_seg, workers):
+            common = (signal.samples.data_ptr(), 0, n_s, spec.data_ptr(), n_fil,
+                      n, seg_plan.tap_len, seg_plan.origin, l_eff, t0,
+                      win_off, lo, hi)
+            tail = (out.data_ptr(), n_s, 0, precision.code, _stream_ptr())
+            if pp.kind == "magnitude_squared":
+                _lib.call("olsb_fused_c2c_abs2_ref", *common, tw.data_ptr(),
+                          *tail)
+            else:
+                _lib.call("olsb_fused_c2c_ref", *common, pp.code,
+                          float(pp.scale), tw.data_ptr(), *tail)
+    return out
 
 
 def _engine_entry(seg_plan: SegmentPlan, pp: PostProcSpec) -> str:

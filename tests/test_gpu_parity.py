@@ -431,3 +431,47 @@ def test_beyond_int32_sample_indices_vs_oracle(oc, mode):
         assert rel_l2_per_filter(got, ref) <= L2_TOL, a
     del out, xs
     torch.cuda.empty_cache()
+
+
+# ---- exact mode: the reference's arithmetic, bit for bit -------------------
+
+@pytest.mark.parametrize("prec", ["single", "double"])
+def test_fused_exact_bit_identical_to_reference(oc, golden, prec):
+    """variant="fused_exact" reproduces the reference's own fp32 / fp64
+    convolve(variant="fused") outputs bit for bit on every cell of the
+    golden grid (first/last segment, M = 1, M = N, N_s < L, origin > 0,
+    real taps on a complex signal, N = 4 .. 4096)."""
+    g = golden["conv"]
+    P = oc.Precision.single if prec == "single" else oc.Precision.double
+    for i, (ns, m, nfil, n, origin, _) in enumerate(CONV_GRID):
+        x, taps = conv_case_inputs(i)
+        p = oc.plan(ns, m, "c2c", origin, n)
+        y = oc.convolve(oc.make_signal(x, "complex", P),
+                        oc.make_filterset(taps, origin, P), p,
+                        variant="fused_exact")
+        ref = torch.from_numpy(g[f"y_{prec}_{i}"])
+        assert torch.equal(y.cpu(), ref), (prec, i)
+
+
+def test_fused_exact_scale_abs2_and_workers(oc):
+    """Exact mode with postproc scale (the reference oracle, itself pinned
+    bit-exact to the reference) and magnitude_squared, split over workers."""
+    ns, m, nfil, n, origin = 20000, 129, 3, 512, 7
+    rng = np.random.default_rng([72, ns])
+    x = rng.standard_normal(ns) + 1j * rng.standard_normal(ns)
+    taps = rng.standard_normal((nfil, m)) + 1j * rng.standard_normal((nfil, m))
+    P = oc.Precision.single
+    p = oc.plan(ns, m, "c2c", origin, n)
+    sig = oc.make_signal(x, "complex", P)
+    fs = oc.make_filterset(taps, origin, P)
+    ys = oc.convolve(sig, fs, p, variant="fused_exact",
+                     postproc=oc.PostProcSpec("scale", 0.3), workers=3)
+    ref = oracle.fused_convolve(x, taps, n, origin, "single", pp_kind=1,
+                                pp_c=0.3)
+    assert torch.equal(ys.cpu(), torch.from_numpy(ref))
+    y = oc.convolve(sig, fs, p, variant="fused_exact")
+    a2 = oc.convolve(sig, fs, p, variant="fused_exact",
+                     postproc=oc.PostProcSpec("magnitude_squared"))
+    yc = y.cpu().numpy()
+    want = yc.real * yc.real + yc.imag * yc.imag   # float32, no FMA
+    assert np.array_equal(a2.cpu().numpy(), want.astype(np.float32))
