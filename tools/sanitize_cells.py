@@ -30,4 +30,10 @@ for n in (8, 16, 64, 256, 512, 1024, 2048, 4096):
                         postproc=ob.PostProcSpec(ppk))
         torch.cuda.synchronize()
         assert torch.isfinite(y).all(), (n, mode, ppk)
+        if mode == "c2c" and ppk in ("none", "magnitude_squared"):
+            y = ob.convolve(ob.make_signal(x, "complex", P),
+                            ob.make_filterset(taps, 0, P), p,
+                            postproc=ob.PostProcSpec(ppk), variant="fused_exact")
+            torch.cuda.synchronize()
+            assert torch.isfinite(y).all(), (n, "exact", ppk)
 print("sanitize cells done")
