@@ -650,6 +650,12 @@ struct FusedArgs {
   const typename V16<R>::type* spec;  // engine layout
   cudaTextureObject_t htex;           // texture over `spec` (H_TEX)
   int n_fil, fchunk, pp_kind;
+  // balanced tail: the first full_items items take groups [0, full_items)
+  // with every filter (fchunk = n_fil); the remaining groups are split into
+  // items of tchunk filters, so the last wave ends within one small item
+  // (0 = plain (group, fchunk) items)
+  long long full_items;
+  int tchunk;
   // segment grid (engine geometry, anchored at global sample 0): segment k
   // reads the zero-extended window x[k*seg_len - t0 + origin, + N) and owns
   // outputs [k*seg_len, (k+1)*seg_len) = in-place samples [t0, t0 + seg_len);
@@ -719,7 +725,29 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   const long long nseg = a.k_hi - a.k_lo;
   const long long ngroups = (nseg + C::SEGS - 1) / C::SEGS;
   const int nfch = (a.n_fil + a.fchunk - 1) / a.fchunk;
-  const long long nitems = ngroups * nfch;
+  const int ntch = a.full_items > 0 ? (a.n_fil + a.tchunk - 1) / a.tchunk : 1;
+  const long long nitems =
+      a.full_items > 0 ? a.full_items + (ngroups - a.full_items) * ntch
+                       : ngroups * nfch;
+  // item -> (segment group, first filter); filters [f_lo, f_lo + width)
+  auto item = [&](long long it, long long& grp, int& f_lo, int& width) {
+    if (a.full_items > 0) {
+      if (it < a.full_items) {
+        grp = it;
+        f_lo = 0;
+        width = a.n_fil;
+      } else {
+        const long long r = it - a.full_items;
+        grp = a.full_items + r / ntch;
+        f_lo = int(r % ntch) * a.tchunk;
+        width = a.tchunk;
+      }
+    } else {
+      grp = it / nfch;
+      f_lo = int(it - grp * nfch) * a.fchunk;
+      width = a.fchunk;
+    }
+  };
 
   if constexpr (C::TMX) {
     if (tid < 32) tmem_alloc<C::TCOLS>(tslot);
@@ -788,7 +816,9 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     }
   };
   if (blockIdx.x < nitems) {
-    const int f0 = int(blockIdx.x % nfch) * a.fchunk;
+    long long g_;
+    int f0, w_;
+    item(blockIdx.x, g_, f0, w_);
     fetch(f0);
   }
 
@@ -796,8 +826,9 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   int xc = 0;
 
   for (long long it = blockIdx.x; it < nitems; it += gridDim.x) {
-    const long long grp = it / nfch;
-    const int fc = int(it - grp * nfch);
+    long long grp;
+    int f_lo, f_w;
+    item(it, grp, f_lo, f_w);
     // s = segment (R2R: segment pair {2s, 2s + 1}) of this thread's group
     const long long s = a.k_lo + grp * C::SEGS + sl;
     const bool live = s < a.k_hi;
@@ -830,7 +861,9 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     // few filters per segment nothing else hides the DRAM latency of the
     // gather at the start of an item
     if (tid == 0 && it + gridDim.x < nitems) {
-      const long long gn = (it + gridDim.x) / nfch;
+      long long gn;
+      int fn_, wn_;
+      item(it + gridDim.x, gn, fn_, wn_);
       const long long sn = a.k_lo + gn * C::SEGS;
       const long long segs = MODE == FMODE_R2R ? 2 * C::SEGS : C::SEGS;
       long long lo = (MODE == FMODE_R2R ? 2 * sn : sn) * a.seg_len - a.t0 + a.origin;
@@ -854,10 +887,14 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
         if (b1 > b0) l2_prefetch(reinterpret_cast<const void*>(b0), uint32_t(b1 - b0));
       }
     }
-    const int f_lo = fc * a.fchunk;
-    const int f_hi = min(a.n_fil, f_lo + a.fchunk);
+    const int f_hi = min(a.n_fil, f_lo + f_w);
     const long long nit = it + gridDim.x;
-    const int f_next_item = nit < nitems ? int(nit % nfch) * a.fchunk : -1;
+    int f_next_item = -1;
+    if (nit < nitems) {
+      long long gn2;
+      int wn2;
+      item(nit, gn2, f_next_item, wn2);
+    }
 
     // ---- segment staging: zero-extended window, top-window layout
     // (_gather, _kernels_nb.py:206-215)

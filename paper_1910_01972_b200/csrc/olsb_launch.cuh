@@ -106,6 +106,18 @@ inline int debug_env() {
   return v;
 }
 
+inline int tail_env() {
+  static int v = [] {
+    const char* e = getenv("OLSB_TAIL_SPLIT");
+    return e ? atoi(e) : 4;
+  }();
+  return v;
+}
+inline bool tail_forced() {
+  static bool v = getenv("OLSB_TAIL_SPLIT") != nullptr;
+  return v;
+}
+
 inline int variant_env() {
   static int v = [] {
     const char* e = getenv("OLSB_VARIANT");
@@ -147,7 +159,25 @@ int launch_fused_cfg(FusedArgs<typename C::R> a, cudaStream_t st) {
                                                               : a.n_fil;
   const long long nseg = a.k_hi - a.k_lo;
   const long long ngroups = (nseg + C::SEGS - 1) / C::SEGS;
-  const long long nitems = ngroups * ((a.n_fil + a.fchunk - 1) / a.fchunk);
+  long long nitems = ngroups * ((a.n_fil + a.fchunk - 1) / a.fchunk);
+  a.full_items = 0;
+  a.tchunk = a.n_fil;
+  // balanced tail: whole waves of full-filter items, then the leftover
+  // groups in items of ~n_fil/4 filters.  It pays only where a CTA that runs
+  // out of work leaves much of its SM idle (<= 2 CTAs/SM, N = 4096) and the
+  // tail is a large part of the launch (< 6 waves): cfg2 N = 4096 0.416 ->
+  // 0.390 ms; with 4 CTAs/SM the other CTAs absorb the idle share and the
+  // extra forward transforms cost more (cfg3 1.72 -> 1.74 ms).
+  // OLSB_TAIL_SPLIT overrides the divisor (0 disables).
+  const int tdiv = tail_env();
+  if (a.fchunk == a.n_fil && tdiv > 0 && a.n_fil >= 2 * tdiv &&
+      (tail_forced() || (C::MINB <= 2 && ngroups < 6LL * resident)) &&
+      ngroups > resident && ngroups % resident != 0) {
+    a.full_items = (ngroups / resident) * resident;
+    a.tchunk = (a.n_fil + tdiv - 1) / tdiv;
+    nitems = a.full_items +
+             (ngroups - a.full_items) * ((a.n_fil + a.tchunk - 1) / a.tchunk);
+  }
   const int grid = int(std::min<long long>(nitems, resident));
   if (grid <= 0) return 0;
   kern<<<grid, C::THREADS, C::f_smem_bytes, st>>>(a);
