@@ -725,13 +725,19 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   const long long nseg = a.k_hi - a.k_lo;
   const long long ngroups = (nseg + C::SEGS - 1) / C::SEGS;
   const int nfch = (a.n_fil + a.fchunk - 1) / a.fchunk;
-  const int ntch = a.full_items > 0 ? (a.n_fil + a.tchunk - 1) / a.tchunk : 1;
-  const long long nitems =
-      a.full_items > 0 ? a.full_items + (ngroups - a.full_items) * ntch
-                       : ngroups * nfch;
+  // the balanced tail is compiled only into the <= 2 CTAs/SM policies (the
+  // launcher never enables it for the others; keeping their item loop
+  // minimal is worth 1.6% at cfg3)
+  constexpr bool TS = C::MINB <= 2;
+  const bool ts = TS && a.full_items > 0;
+  const int ntch = ts ? (a.n_fil + a.tchunk - 1) / a.tchunk : 1;
+  long long nitems = ngroups * nfch;
+  if constexpr (TS) {
+    if (ts) nitems = a.full_items + (ngroups - a.full_items) * ntch;
+  }
   // item -> (segment group, first filter); filters [f_lo, f_lo + width)
   auto item = [&](long long it, long long& grp, int& f_lo, int& width) {
-    if (a.full_items > 0) {
+    if (TS && ts) {
       if (it < a.full_items) {
         grp = it;
         f_lo = 0;
@@ -816,9 +822,12 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     }
   };
   if (blockIdx.x < nitems) {
-    long long g_;
-    int f0, w_;
-    item(blockIdx.x, g_, f0, w_);
+    int f0 = int(blockIdx.x % nfch) * a.fchunk;
+    if constexpr (TS) {
+      long long g_;
+      int w_;
+      item(blockIdx.x, g_, f0, w_);
+    }
     fetch(f0);
   }
 
@@ -826,9 +835,9 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   int xc = 0;
 
   for (long long it = blockIdx.x; it < nitems; it += gridDim.x) {
-    long long grp;
-    int f_lo, f_w;
-    item(it, grp, f_lo, f_w);
+    long long grp = it / nfch;
+    int f_lo = int(it - grp * nfch) * a.fchunk, f_w = a.fchunk;
+    if constexpr (TS) item(it, grp, f_lo, f_w);
     // s = segment (R2R: segment pair {2s, 2s + 1}) of this thread's group
     const long long s = a.k_lo + grp * C::SEGS + sl;
     const bool live = s < a.k_hi;
@@ -861,9 +870,11 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     // few filters per segment nothing else hides the DRAM latency of the
     // gather at the start of an item
     if (tid == 0 && it + gridDim.x < nitems) {
-      long long gn;
-      int fn_, wn_;
-      item(it + gridDim.x, gn, fn_, wn_);
+      long long gn = (it + gridDim.x) / nfch;
+      if constexpr (TS) {
+        int fn_, wn_;
+        item(it + gridDim.x, gn, fn_, wn_);
+      }
       const long long sn = a.k_lo + gn * C::SEGS;
       const long long segs = MODE == FMODE_R2R ? 2 * C::SEGS : C::SEGS;
       long long lo = (MODE == FMODE_R2R ? 2 * sn : sn) * a.seg_len - a.t0 + a.origin;
@@ -889,11 +900,13 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     }
     const int f_hi = min(a.n_fil, f_lo + f_w);
     const long long nit = it + gridDim.x;
-    int f_next_item = -1;
-    if (nit < nitems) {
-      long long gn2;
-      int wn2;
-      item(nit, gn2, f_next_item, wn2);
+    int f_next_item = nit < nitems ? int(nit % nfch) * a.fchunk : -1;
+    if constexpr (TS) {
+      if (nit < nitems) {
+        long long gn2;
+        int wn2;
+        item(nit, gn2, f_next_item, wn2);
+      }
     }
 
     // ---- segment staging: zero-extended window, top-window layout

@@ -171,7 +171,7 @@ int launch_fused_cfg(FusedArgs<typename C::R> a, cudaStream_t st) {
   // OLSB_TAIL_SPLIT overrides the divisor (0 disables).
   const int tdiv = tail_env();
   if (a.fchunk == a.n_fil && tdiv > 0 && a.n_fil >= 2 * tdiv &&
-      (tail_forced() || (C::MINB <= 2 && ngroups < 6LL * resident)) &&
+      C::MINB <= 2 && (tail_forced() || ngroups < 6LL * resident) &&
       ngroups > resident && ngroups % resident != 0) {
     a.full_items = (ngroups / resident) * resident;
     a.tchunk = (a.n_fil + tdiv - 1) / tdiv;
