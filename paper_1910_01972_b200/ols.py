@@ -392,32 +392,45 @@ def _fused_exact(signal, filters, seg_plan, pp, precision, l_eff, t0,
     """variant="fused_exact": the fused engine with the reference's
     arithmetic (olsb_fused_c2c_ref): outputs bit-identical to the
     reference's fp32 / fp64 ``convolve(variant="fused")``."""
-    if not signal.samples.is_cuda or (out is not None and not out.is_cuda):
-        raise ValueError("variant 'fused_exact' runs on device-resident "
-                         "signal and output")
+    host_out = out is not None and not out.is_cuda
+    if not signal.samples.is_cuda and not host_out:
+        raise ValueError("a host-resident signal needs a host `out` "
+                         "(streaming path)")
     n, n_s, n_fil = seg_plan.fft_len, signal.length, filters.n_filters
-    dev = signal.samples.device
+    dev = (signal.samples.device if signal.samples.is_cuda
+           else filters.taps.device if filters.taps.is_cuda
+           else torch.device("cuda", torch.cuda.current_device()))
     tw = _ref_twiddles(n, precision, dev)
     taps = filters.taps.to(device=dev, dtype=precision.torch_complex)
     taps = taps.contiguous()
     spec = torch.empty((n_fil, n), dtype=precision.torch_complex, device=dev)
-    if out is None:
-        out = torch.empty((n_fil, n_s), dtype=out_dtype, device=dev)
     with torch.cuda.device(dev):
         _lib.call("olsb_filter_spectra_c2c_ref", taps.data_ptr(), n_fil,
                   seg_plan.tap_len, n, tw.data_ptr(), None, spec.data_ptr(),
                   precision.code, _stream_ptr())
+
+    def launch(x, f0, f1, dst, ld, stream, lo=0, hi=n_seg):
+        common = (x.data_ptr(), 0, n_s, spec[f0].data_ptr(), f1 - f0, n,
+                  seg_plan.tap_len, seg_plan.origin, l_eff, t0, win_off, lo, hi)
+        tail = (dst.data_ptr(), ld, 0, precision.code, stream)
+        if pp.kind == "magnitude_squared":
+            _lib.call("olsb_fused_c2c_abs2_ref", *common, tw.data_ptr(), *tail)
+        else:
+            _lib.call("olsb_fused_c2c_ref", *common, pp.code, float(pp.scale),
+                      tw.data_ptr(), *tail)
+
+    if host_out:
+        # host streaming in chunks of whole output rows (contiguous D2H)
+        row = n_s * out.element_size()
+        fc = max(1, min(_STREAM_TILE // row, max(1, n_fil // 3)))
+        return _fused_streaming_rows(
+            signal, spec, seg_plan, pp, precision, out, fc,
+            launch=lambda x, f0, f1, ob, st: launch(x, f0, f1, ob, n_s, st))
+    if out is None:
+        out = torch.empty((n_fil, n_s), dtype=out_dtype, device=dev)
+    with torch.cuda.device(dev):
         for lo, hi in _chunk_bounds(n_seg, workers):
-            common = (signal.samples.data_ptr(), 0, n_s, spec.data_ptr(), n_fil,
-                      n, seg_plan.tap_len, seg_plan.origin, l_eff, t0,
-                      win_off, lo, hi)
-            tail = (out.data_ptr(), n_s, 0, precision.code, _stream_ptr())
-            if pp.kind == "magnitude_squared":
-                _lib.call("olsb_fused_c2c_abs2_ref", *common, tw.data_ptr(),
-                          *tail)
-            else:
-                _lib.call("olsb_fused_c2c_ref", *common, pp.code,
-                          float(pp.scale), tw.data_ptr(), *tail)
+            launch(signal.samples, 0, n_fil, out, n_s, _stream_ptr(), lo, hi)
     return out
 
 
@@ -552,8 +565,10 @@ def _fused_streaming(signal, spec_dev, seg_plan, pp, precision, l_eff, t0,
 
 
 def _fused_streaming_rows(signal, spec_dev, seg_plan, pp, precision, out,
-                          fc):
-    """Host-memory path chunked by filters (see _fused_streaming)."""
+                          fc, launch=None):
+    """Host-memory path chunked by filters (see _fused_streaming).
+    ``launch(x_dev, f0, f1, obuf, stream)`` replaces the default range
+    launch (exact mode)."""
     n_s = signal.length
     n_fil = spec_dev.shape[0]
     dev = spec_dev.device
@@ -577,9 +592,12 @@ def _fused_streaming_rows(signal, spec_dev, seg_plan, pp, precision, out,
             k = i % nslot
             st = streams[k]
             with torch.cuda.stream(st):
-                fused_range_launch(xdev, 0, n_s, spec_dev[f0:f1], f1 - f0,
-                                   seg_plan, 0, n_s, pp, obuf[k], n_s, 0,
-                                   precision, st.cuda_stream)
+                if launch is not None:
+                    launch(xdev, f0, f1, obuf[k], st.cuda_stream)
+                else:
+                    fused_range_launch(xdev, 0, n_s, spec_dev[f0:f1], f1 - f0,
+                                       seg_plan, 0, n_s, pp, obuf[k], n_s, 0,
+                                       precision, st.cuda_stream)
                 out[f0:f1].copy_(obuf[k][:f1 - f0], non_blocking=True)
         for s in streams:
             ready.wait_stream(s)

@@ -475,3 +475,28 @@ def test_fused_exact_scale_abs2_and_workers(oc):
     yc = y.cpu().numpy()
     want = yc.real * yc.real + yc.imag * yc.imag   # float32, no FMA
     assert np.array_equal(a2.cpu().numpy(), want.astype(np.float32))
+
+
+def test_fused_exact_host_streaming(oc, golden):
+    """Exact mode from a pinned host signal into a pinned host output (row
+    chunks, contiguous D2H) equals the reference's fp32 output bit for bit."""
+    g = golden["conv"]
+    from paper_1910_01972_b200 import ols as ols_mod
+    for i in (10, 17, 18):
+        ns, m, nfil, n, origin, _ = CONV_GRID[i]
+        x, taps = conv_case_inputs(i)
+        P = oc.Precision.single
+        p = oc.plan(ns, m, "c2c", origin, n)
+        hsig = oc.make_signal(
+            torch.from_numpy(x.astype(np.complex64)).pin_memory(), "complex",
+            P, device="cpu")
+        host = torch.full((nfil, ns), float("nan"),
+                          dtype=torch.complex64).pin_memory()
+        tile = ols_mod._STREAM_TILE
+        try:
+            ols_mod._STREAM_TILE = ns * 8      # one row per chunk
+            oc.convolve(hsig, oc.make_filterset(taps, origin, P), p,
+                        variant="fused_exact", out=host)
+        finally:
+            ols_mod._STREAM_TILE = tile
+        assert torch.equal(host, torch.from_numpy(g[f"y_single_{i}"])), i
