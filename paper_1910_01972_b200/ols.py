@@ -410,6 +410,8 @@ def _fused_exact(signal, filters, seg_plan, pp, precision, l_eff, t0,
                   precision.code, _stream_ptr())
 
     def launch(x, f0, f1, dst, ld, stream, lo=0, hi=n_seg):
+        if f1 <= f0:
+            return
         common = (x.data_ptr(), 0, n_s, spec[f0].data_ptr(), f1 - f0, n,
                   seg_plan.tap_len, seg_plan.origin, l_eff, t0, win_off, lo, hi)
         tail = (dst.data_ptr(), ld, 0, precision.code, stream)
