@@ -29,6 +29,9 @@ CFG = {
     "cfg4_m32_f1": (1 << 24, 32, 1, 128),
     "cfg4_m16_f8": (1 << 24, 16, 8, 64),
     "cfg4_m8_f4": (1 << 24, 8, 4, 64),
+    "cfg4_m8_f2": (1 << 24, 8, 2, 64),
+    "cfg1_f2": (1 << 20, 64, 2, 1024),
+    "cfg1_f4": (1 << 20, 64, 4, 1024),
     # cfg5's per-GPU share at 8 GPUs (2^30 / 8 samples, 64 filters M=512)
     "cfg5_shard8": (1 << 27, 512, 64, 4096),
     # real (r2r) path on the same shapes
