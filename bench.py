@@ -112,53 +112,67 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_baseline(sample_ns: int, repeats: int = 2):
-    """The oracle's C restatement of the reference fused path (fp32,
-    _kernels_nb.py:265-285), all host threads, on the first `sample_ns`
-    samples of the cfg3 workload with all 96 filters."""
-    import oracle
-    from cases import gen_inputs
-    x, taps = gen_inputs(NS, M, NFIL)
-    x = x[:sample_ns].astype(np.complex64)
-    taps = taps.astype(np.complex64)
-    threads = oracle.max_threads()
-    oracle.fused_convolve(x[:1 << 14], taps, NFFT, 0, "single", threads)
-    ts = []
-    for _ in range(repeats):
+class CpuReference:
+    """The reference's CPU path on the host cores: the oracle's C restatement
+    of the reference fused kernel (fp32, _kernels_nb.py:265-285, pinned
+    bit-exact to the reference's own outputs), split into contiguous segment
+    ranges over all host threads like ols.py:212-225.  The sample is the
+    FULL cfg3 workload (2^23 samples x 96 filters, N = 2048), timed per call
+    like the reference bench times a cell (cli.py:173-181, 223-241)."""
+
+    def __init__(self):
+        import oracle
+        from cases import gen_inputs
+        x, taps = gen_inputs(NS, M, NFIL)
+        self.oracle = oracle
+        self.x = x.astype(np.complex64)
+        self.taps = taps.astype(np.complex64)
+        self.threads = oracle.max_threads()
+        oracle.fused_convolve(self.x[:1 << 14], self.taps, NFFT, 0, "single",
+                              self.threads)
+
+    def run_once(self) -> float:
         t0 = time.perf_counter()
-        oracle.fused_convolve(x, taps, NFFT, 0, "single", threads)
-        ts.append(time.perf_counter() - t0)
-    t = statistics.median(ts)
-    return {"value": sample_ns * NFIL / t, "unit": "samples/s",
-            "cores": threads, "kind": "port",
-            "sample": f"first {sample_ns} samples x {NFIL} filters of the "
-                      f"cfg3 signal, median of {repeats}",
-            "seconds": t}
+        self.oracle.fused_convolve(self.x, self.taps, NFFT, 0, "single",
+                                   self.threads)
+        return time.perf_counter() - t0
+
+    def describe(self, secs: float, repeats: int) -> dict:
+        return {"value": NS * NFIL / secs, "unit": "samples/s",
+                "cores": self.threads, "kind": "port",
+                "sample": f"full cfg3 workload: {NS} samples x {NFIL} filters "
+                          f"(M={M}, N={NFFT}), median of {repeats}",
+                "same_config": True}
+
+
+def cpu_baseline(repeats: int = 2):
+    ref = CpuReference()
+    t = statistics.median(ref.run_once() for _ in range(repeats))
+    return ref.describe(t, repeats)
 
 
 def run_reference(args, rank: int):
     """--impl reference: the reference's CPU path (C port of its numba
-    kernels, oracle/) on the host cores, same metric and config."""
+    kernels, oracle/) on the host cores, same metric and config: every step
+    is one full cfg3 convolution."""
     if rank != 0:
         return
-    sample = 1 << 21
+    ref = CpuReference()
     for _ in range(args.warmup):
-        cpu_baseline(sample, repeats=1)
-    vals = []
-    for _ in range(args.steps):
-        vals.append(cpu_baseline(sample, repeats=1))
-    v = statistics.median(r["value"] for r in vals)
-    secs = statistics.median(r["seconds"] for r in vals)
-    cb = dict(vals[0])
-    cb["value"] = v
-    cb.pop("seconds", None)
+        ref.run_once()
+    secs_all = [ref.run_once() for _ in range(args.steps)]
+    secs = statistics.median(secs_all)
+    cb = ref.describe(secs, args.steps)
+    v = cb["value"]
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": secs * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "complex64 (fp32)",
         "data": "synthetic (reference generator convention, cli.py:41-55)",
-        "config": {"workload": WORKLOAD, "sample_per_step": cb["sample"],
+        "config": {"workload": WORKLOAD, "signal_samples": NS,
+                   "filters": NFIL, "taps": M, "fft_len": NFFT,
+                   "sample_per_step": cb["sample"],
                    "parallelism": "host threads (pthreads over segments)"},
         "cpu_baseline": cb,
         "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0,
@@ -383,8 +397,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            cpu = cpu_baseline(1 << 21)
-            cpu.pop("seconds", None)
+            cpu = cpu_baseline()
         except Exception as exc:  # the oracle needs gcc-built oracle/build
             cpu = {"error": str(exc)}
 
