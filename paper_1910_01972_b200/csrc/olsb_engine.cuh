@@ -40,6 +40,15 @@ struct V16<double> {
   static constexpr int per = 1;
 };
 
+// Engine layout of filter spectra: 16-byte vector u (in-place samples
+// 16 t + 2u, +1) of E = 16 thread t at index f * N/2 + spec_vec(t, u) =
+// u * T + t: the four threads of a texture quad read 64 contiguous bytes
+// (the warp-per-segment kernel of olsb_w64.cuh reads the same layout).
+template <class R, int LOGN>
+__host__ __device__ constexpr int spec_vec(int t, int u) {
+  return u * (Geo<LOGN>::T) + t;
+}
+
 // How the fused kernel fetches filter spectra:
 enum HMode : int {
   H_LDG = 0,  // read through L1 with __ldg at the multiply (fp64 policy)
@@ -814,10 +823,10 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   float4 hn[C::PREF ? C::VPT : 1];
   auto fetch = [&](int f) {
     if constexpr (C::PREF) {
-      const int hb = ((C::ABL & 8) ? (f & 1) : f) * (C::VPT * T) + t;
+      const int hb = ((C::ABL & 8) ? (f & 1) : f) * (C::VPT * T);
       sfor<0, C::VPT>([&](auto uc) {
         constexpr int u = decltype(uc)::value;
-        hn[u] = tex1Dfetch<float4>(a.htex, hb + u * T);
+        hn[u] = tex1Dfetch<float4>(a.htex, hb + spec_vec<R, LOGN>(t, u));
       });
     }
   };
@@ -982,16 +991,16 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
         });
         if (f_next >= 0) fetch(f_next);
       } else if constexpr (C::HM == H_TEX) {
-        const int hb = f * (C::VPT * T) + t;
+        const int hb = f * (C::VPT * T);
         sfor<0, C::VPT>([&](auto uc) {
           constexpr int u = decltype(uc)::value;
-          mulh(u, tex1Dfetch<float4>(a.htex, hb + u * T));
+          mulh(u, tex1Dfetch<float4>(a.htex, hb + spec_vec<R, LOGN>(t, u)));
         });
       } else {
-        const typename V16<R>::type* hs = a.spec + (size_t(f) * C::VPT) * T + t;
+        const typename V16<R>::type* hs = a.spec + (size_t(f) * C::VPT) * T;
         sfor<0, C::VPT>([&](auto uc) {
           constexpr int u = decltype(uc)::value;
-          const auto h = __ldg(hs + u * T);
+          const auto h = __ldg(hs + spec_vec<R, LOGN>(t, u));
           if constexpr (V16<R>::per == 2) {
             mulh(u, h);
           } else {
@@ -1182,16 +1191,16 @@ __global__ void __launch_bounds__(C::THREADS)
         for (int e = 0; e < E; ++e) o[e] = x[e];
       }
       if (a.out_dev) {
-        typename V16<R>::type* o = a.out_dev + size_t(r) * C::VPT * T + t;
+        typename V16<R>::type* o = a.out_dev + size_t(r) * C::VPT * T;
         if constexpr (!C::dbl) {
 #pragma unroll
           for (int u = 0; u < C::VPT; ++u)
-            o[u * T] = make_float4(x[2 * u].re, x[2 * u].im, x[2 * u + 1].re,
+            o[spec_vec<R, C::LOGN>(t, u)] = make_float4(x[2 * u].re, x[2 * u].im, x[2 * u + 1].re,
                                    x[2 * u + 1].im);
         } else {
 #pragma unroll
           for (int u = 0; u < C::VPT; ++u)
-            o[u * T] = make_double2(x[u].re, x[u].im);
+            o[spec_vec<R, C::LOGN>(t, u)] = make_double2(x[u].re, x[u].im);
         }
       }
     }
@@ -1259,7 +1268,8 @@ __global__ void perm_to_dev_kernel(const Cpx<typename C::R>* perm,
     const int u = rem / T, t = rem % T;
     const Cpx<R>* s = perm + r * C::G::N + t * C::E + u * per;
     if constexpr (per == 2) {
-      dev[i] = make_float4(s[0].re, s[0].im, s[1].re, s[1].im);
+      dev[r * (VPT * T) + spec_vec<R, C::LOGN>(t, u)] =
+          make_float4(s[0].re, s[0].im, s[1].re, s[1].im);
     } else {
       dev[i] = make_double2(s[0].re, s[0].im);
     }

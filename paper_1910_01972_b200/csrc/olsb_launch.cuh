@@ -14,6 +14,7 @@
 
 #include "olsb.h"
 #include "olsb_engine.cuh"
+#include "olsb_w64.cuh"
 
 namespace olsb {
 
@@ -207,9 +208,59 @@ using SingleFilterPolicy =
          DefaultPolicy<R, LOGN>::type::NBUF, DefaultPolicy<R, LOGN>::type::HM,
          1, DefaultPolicy<R, LOGN>::type::MINB, 0, 0>;
 
+// warp-per-segment engine for N = 2048 (olsb_w64.cuh), selected with
+// OLSB_W64=1.  Not the default: at 8 warps/SM (252 registers) its FP core
+// alone takes 1.32 ms on cfg3 against the E = 16 engine's 1.05 ms, so
+// halving the exchange traffic and dropping the CTA barriers only reaches
+// parity (1.68 ms)
+inline int w64_env() {
+  static int v = [] {
+    const char* e = getenv("OLSB_W64");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+template <int WPC, int MINB, int MODE>
+int launch_w64_cfg(FusedArgs<float> a, cudaStream_t st) {
+  auto kern = w64::fused_w64_kernel<WPC, MINB, MODE>;
+  constexpr size_t smem = size_t(WPC) * w64::BUF * sizeof(Cpx<float>) + 16;
+  int resident = 0;
+  int rc = prepare(kern, smem, WPC * 32, &resident);
+  if (rc) return rc;
+  // TMEM-allocating kernels: the occupancy API reports 1 CTA/SM
+  resident = std::max(resident, MINB * num_sms());
+  rc = spectra_texture(a.spec, size_t(a.n_fil) * 1024 * 16, &a.htex);
+  if (rc) return rc;
+  const long long nseg = a.k_hi - a.k_lo;
+  const long long warps = (long long)resident * WPC;
+  // whole waves of full-filter items, then the leftover segments in items
+  // of ~n_fil/8 filters so every warp finishes within one small item
+  a.full_items = nseg;
+  a.tchunk = a.n_fil;
+  if (nseg % warps != 0 && a.n_fil >= 2) {
+    a.full_items = (nseg / warps) * warps;
+    const int tdiv = std::min(8, a.n_fil);
+    a.tchunk = (a.n_fil + tdiv - 1) / tdiv;
+  }
+  const long long ntch = (a.n_fil + a.tchunk - 1) / a.tchunk;
+  const long long nitems = a.full_items + (nseg - a.full_items) * ntch;
+  const long long grid = std::min<long long>((nitems + WPC - 1) / WPC, resident);
+  if (grid <= 0) return 0;
+  kern<<<int(grid), WPC * 32, smem, st>>>(a);
+  return int(cudaGetLastError());
+}
+
 template <class R, int LOGN>
 int launch_fused(FusedArgs<R> a, int mode, cudaStream_t st) {
   using D = typename DefaultPolicy<R, LOGN>::type;
+  if constexpr (std::is_same<R, float>::value && LOGN == 11) {
+    if (!a.xtw && variant_env() < 0 && w64_env() &&
+        (a.pp_kind == OLSB_PP_NONE || a.pp_kind == OLSB_PP_SCALE)) {
+      if (mode == FMODE_C2C) return launch_w64_cfg<4, 2, FMODE_C2C>(a, st);
+      if (mode == FMODE_ABS2) return launch_w64_cfg<4, 2, FMODE_ABS2>(a, st);
+    }
+  }
   if constexpr (std::is_same<R, float>::value) {
     if (a.n_fil == 1 && !a.xtw && variant_env() < 0) {
       using S = SingleFilterPolicy<R, LOGN>;
