@@ -108,7 +108,9 @@ int olsb_fused_c2c(const void* x, int64_t x_base, int64_t n_s,
  * grid, anchored at global sample 0, so results are bit-identical for any
  * partition of [0, n_s) into ranges.  `x`, `x_base`, `n_s`, `out`, `out_ld`,
  * `out_base` as in olsb_fused_c2c; the input samples a call reads are
- * [x_lo, x_hi) of olsb_input_extent (clipped to [0, n_s)). */
+ * [x_lo, x_hi) of olsb_input_extent (clipped to [0, n_s)).  pp_kind
+ * OLSB_PP_MAG2 selects the |y|^2 epilogue of olsb_fused_c2c_abs2: `out` is
+ * then REAL. */
 int olsb_fused_c2c_range(const void* x, int64_t x_base, int64_t n_s,
                          const void* spectra_dev, int n_fil, int n, int m,
                          int origin, int64_t g_lo, int64_t g_hi, int pp_kind,

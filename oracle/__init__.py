@@ -53,7 +53,7 @@ def lib():
                 getattr(L, f"ols_dit_inv_batch_{sfx}").argtypes = [c_vp, c_int, c_int, c_vp]
                 getattr(L, f"ols_fused_c2c_{sfx}").argtypes = [
                     c_vp, c_i64, c_vp, c_int, c_int, c_vp, c_vp, c_i64, c_i64,
-                    c_i64, c_i64, c_i64, c_int, R, c_vp, c_int]
+                    c_i64, c_i64, c_i64, c_int, ctypes.c_double, c_vp, c_int]
             L.ols_direct_d.argtypes = [c_vp, c_i64, c_vp, c_int, c_int, c_int,
                                        c_vp, c_int]
             L.ols_oracle_max_threads.restype = c_int

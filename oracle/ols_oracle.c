@@ -158,7 +158,7 @@ static void run_chunks(int threads, int64_t lo0, int64_t hi0, chunk_fn fn,
                                 const cpx_##SFX* spectra, int n_fil, int n,   \
                                 const R* tw, const R* twc, int64_t l_eff,     \
                                 int64_t t0, int64_t win_off, int64_t seg_lo,  \
-                                int64_t seg_hi, int pp_kind, R pp_c,          \
+                                int64_t seg_hi, int pp_kind, double pp_c,     \
                                 cpx_##SFX* out, cpx_##SFX* buf,               \
                                 cpx_##SFX* spec_buf) {                        \
     for (int64_t s = seg_lo; s < seg_hi; ++s) {                               \
@@ -185,9 +185,11 @@ static void run_chunks(int threads, int64_t lo0, int64_t hi0, chunk_fn fn,
         if (pp_kind == 0) {                                                   \
           for (int64_t j = 0; j < span; ++j) row[g0 + j] = buf[t0 + j];       \
         } else {                                                              \
+          /* _store kind 1: Python-float pp_c x complex64 promotes to     \
+             complex128, rounded once into the output (ols.py _store) */  \
           for (int64_t j = 0; j < span; ++j) {                                \
-            row[g0 + j].re = pp_c * buf[t0 + j].re;                           \
-            row[g0 + j].im = pp_c * buf[t0 + j].im;                           \
+            row[g0 + j].re = (R)(pp_c * (double)buf[t0 + j].re);              \
+            row[g0 + j].im = (R)(pp_c * (double)buf[t0 + j].im);              \
           }                                                                   \
         }                                                                     \
       }                                                                       \
@@ -198,7 +200,7 @@ static void run_chunks(int threads, int64_t lo0, int64_t hi0, chunk_fn fn,
     const R *x, *spectra, *tw, *twc;                                          \
     int64_t n_s, l_eff, t0, win_off;                                          \
     int n_fil, n, pp_kind;                                                    \
-    R pp_c;                                                                   \
+    double pp_c;                                                              \
     R* out;                                                                   \
   } fused_ctx_##SFX;                                                          \
                                                                               \
@@ -220,7 +222,7 @@ static void run_chunks(int threads, int64_t lo0, int64_t hi0, chunk_fn fn,
                            int n_fil, int n, const R* tw, const R* twc,       \
                            int64_t l_eff, int64_t t0, int64_t win_off,        \
                            int64_t seg_lo, int64_t seg_hi, int pp_kind,       \
-                           R pp_c, R* out, int threads) {                     \
+                           double pp_c, R* out, int threads) {                \
     fused_ctx_##SFX c = {x,     spectra, tw,      twc,     n_s, l_eff,        \
                          t0,    win_off, n_fil,   n,       pp_kind,           \
                          pp_c,  out};                                         \

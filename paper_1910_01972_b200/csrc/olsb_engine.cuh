@@ -658,6 +658,7 @@ struct FusedArgs {
   long long x_base, n_s;
   const typename V16<R>::type* spec;  // engine layout
   cudaTextureObject_t htex;           // texture over `spec` (H_TEX)
+  int hoff;  // float4 offset of `spec` from the texture base (alignment)
   int n_fil, fchunk, pp_kind;
   // balanced tail: the first full_items items take groups [0, full_items)
   // with every filter (fchunk = n_fil); the remaining groups are split into
@@ -672,6 +673,7 @@ struct FusedArgs {
   int t0, origin;
   long long seg_len, k_lo, k_hi, g_lo, g_hi;
   R pp_c;
+  double pp_cd;  // pp_c as the caller passed it (exact mode's _store)
   Cpx<R>* out;
   long long out_ld, out_base;
   int dbg;  // tuning: bit 0 = predicate off the output stores
@@ -823,7 +825,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   float4 hn[C::PREF ? C::VPT : 1];
   auto fetch = [&](int f) {
     if constexpr (C::PREF) {
-      const int hb = ((C::ABL & 8) ? (f & 1) : f) * (C::VPT * T);
+      const int hb = a.hoff + ((C::ABL & 8) ? (f & 1) : f) * (C::VPT * T);
       sfor<0, C::VPT>([&](auto uc) {
         constexpr int u = decltype(uc)::value;
         hn[u] = tex1Dfetch<float4>(a.htex, hb + spec_vec<R, LOGN>(t, u));
@@ -885,7 +887,10 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
         item(it + gridDim.x, gn, fn_, wn_);
       }
       const long long sn = a.k_lo + gn * C::SEGS;
-      const long long segs = MODE == FMODE_R2R ? 2 * C::SEGS : C::SEGS;
+      // the next group's live segments only: its window stays inside the
+      // input extent the caller guarantees for [k_lo, k_hi)
+      const long long nl = a.k_hi - sn < C::SEGS ? a.k_hi - sn : C::SEGS;
+      const long long segs = MODE == FMODE_R2R ? 2 * nl : nl;
       long long lo = (MODE == FMODE_R2R ? 2 * sn : sn) * a.seg_len - a.t0 + a.origin;
       long long hi = lo + (segs - 1) * a.seg_len + G::N;
       lo = lo > 0 ? lo : 0;
@@ -991,7 +996,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
         });
         if (f_next >= 0) fetch(f_next);
       } else if constexpr (C::HM == H_TEX) {
-        const int hb = f * (C::VPT * T);
+        const int hb = a.hoff + f * (C::VPT * T);
         sfor<0, C::VPT>([&](auto uc) {
           constexpr int u = decltype(uc)::value;
           mulh(u, tex1Dfetch<float4>(a.htex, hb + spec_vec<R, LOGN>(t, u)));
@@ -1035,12 +1040,17 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
         }
       });
       if constexpr (XR) {
-        // dit_inv's final 1/N (exact: a power of two), then _store's pp_c
+        // dit_inv's final 1/N (exact: a power of two), then _store's pp_c:
+        // the reference multiplies a Python float by the complex64 sample,
+        // i.e. in double precision, and rounds once into the output
+        // (_kernels_nb.py:223-225)
         const bool scl = a.pp_kind == OLSB_PP_SCALE;
 #pragma unroll
         for (int e = 0; e < E; ++e) {
           Cpx<R> v{mul_rn(y[e].re, inv_n), mul_rn(y[e].im, inv_n)};
-          if (scl) v = Cpx<R>{mul_rn(a.pp_c, v.re), mul_rn(a.pp_c, v.im)};
+          if (scl)
+            v = Cpx<R>{R(__dmul_rn(a.pp_cd, double(v.re))),
+                       R(__dmul_rn(a.pp_cd, double(v.im)))};
           y[e] = v;
         }
       }

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <vector>
 
 #include "olsb.h"
 #include "olsb_launch.cuh"
@@ -63,8 +64,14 @@ void prepared_store(const void* kernel, int resident) {
 }
 
 // Texture objects over engine-layout spectra (H_TEX), cached per
-// (device, pointer, size); creating one costs microseconds, so a FilterSet
-// reused across calls pays it once.
+// (device, base, size); creating one costs microseconds, so a FilterSet
+// reused across calls pays it once.  Entries are never destroyed: a launch
+// still in flight on any stream, or a CUDA graph captured by
+// Executor.graph(), may hold the handle, and destroying it would need a
+// device-wide sync that is illegal during stream capture.  A linear texture
+// is only a (pointer, size) descriptor, so an entry stays valid when its
+// allocation is freed and the address reused; the cache grows by one small
+// descriptor per distinct spectra range a process ever launches with.
 struct TexKey {
   int dev;
   const void* ptr;
@@ -72,19 +79,16 @@ struct TexKey {
   cudaTextureObject_t tex;
 };
 static std::mutex g_tex_mu;
-constexpr int kTexCache = 128;
-static TexKey g_tex_cache[kTexCache];
-static int g_tex_n = 0;
+static std::vector<TexKey> g_tex_cache;
 
 int spectra_texture(const void* ptr, size_t bytes,
                            cudaTextureObject_t* out) {
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lk(g_tex_mu);
-  for (int i = 0; i < g_tex_n; ++i) {
-    if (g_tex_cache[i].dev == dev && g_tex_cache[i].ptr == ptr &&
-        g_tex_cache[i].bytes == bytes) {
-      *out = g_tex_cache[i].tex;
+  for (const TexKey& k : g_tex_cache) {
+    if (k.dev == dev && k.ptr == ptr && k.bytes == bytes) {
+      *out = k.tex;
       return 0;
     }
   }
@@ -98,18 +102,7 @@ int spectra_texture(const void* ptr, size_t bytes,
   cudaTextureObject_t tex = 0;
   cudaError_t e = cudaCreateTextureObject(&tex, &rd, &td, nullptr);
   if (e != cudaSuccess) return int(e);
-  // a freed-and-reused allocation with the same address keeps a valid
-  // descriptor (linear textures hold only pointer + size)
-  if (g_tex_n == kTexCache) {
-    // the oldest object may still be read by a kernel in flight on any
-    // stream: drain the device before destroying it (rare: only after
-    // kTexCache distinct spectra buffers)
-    cudaDeviceSynchronize();
-    cudaDestroyTextureObject(g_tex_cache[0].tex);
-    for (int i = 1; i < kTexCache; ++i) g_tex_cache[i - 1] = g_tex_cache[i];
-    g_tex_n = kTexCache - 1;
-  }
-  g_tex_cache[g_tex_n++] = TexKey{dev, ptr, bytes, tex};
+  g_tex_cache.push_back(TexKey{dev, ptr, bytes, tex});
   *out = tex;
   return 0;
 }
@@ -338,6 +331,7 @@ static int fused_range(int mode, const void* x, int64_t x_base, int64_t n_s,
       a.g_lo = g_lo;
       a.g_hi = g_hi;
       a.pp_c = R(pp_c);
+      a.pp_cd = pp_c;
       a.out = static_cast<Cpx<R>*>(out);
       a.outr = static_cast<R*>(out);
       a.out_ld = out_ld;
@@ -445,6 +439,11 @@ int olsb_fused_c2c_range(const void* x, int64_t x_base, int64_t n_s,
                          double pp_c, void* out, int64_t out_ld,
                          int64_t out_base, int precision, void* stream) {
   if (m < 1 || m > n || origin < 0 || origin >= m) return OLSB_E_BAD_ARG;
+  // magnitude_squared: the |y|^2 epilogue into a REAL out
+  if (pp_kind == OLSB_PP_MAG2)
+    return fused_range(FMODE_ABS2, x, x_base, n_s, spectra_dev, n_fil, n,
+                       m - 1, origin, n - m + 1, g_lo, g_hi, OLSB_PP_NONE, 1.0,
+                       out, out_ld, out_base, precision, stream);
   return fused_range(FMODE_C2C, x, x_base, n_s, spectra_dev, n_fil, n, m - 1,
                      origin, n - m + 1, g_lo, g_hi, pp_kind, pp_c, out, out_ld,
                      out_base, precision, stream);

@@ -54,6 +54,25 @@ extern int g_filter_chunk;
 // texture object over engine-layout spectra (cached; olsb_kernels.cu)
 int spectra_texture(const void* ptr, size_t bytes, cudaTextureObject_t* out);
 
+// Bind the spectra of a launch: linear textures need a textureAlignment-
+// aligned base, and callers may pass a sub-range of a filter bank (the
+// streaming path's row chunks), so the texture starts at the aligned-down
+// address and the kernel adds the float4 offset.
+template <class R>
+int bind_spectra(FusedArgs<R>& a, size_t bytes) {
+  static int align = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrTextureAlignment, dev);
+    return v > 0 ? v : 512;
+  }();
+  const uintptr_t p = reinterpret_cast<uintptr_t>(a.spec);
+  const uintptr_t base = p & ~uintptr_t(align - 1);
+  a.hoff = int((p - base) / 16);
+  return spectra_texture(reinterpret_cast<const void*>(base), bytes + (p - base),
+                         &a.htex);
+}
+
 // default fused-kernel policy per (precision, N)
 template <class R, int LOGN>
 struct DefaultPolicy {
@@ -153,7 +172,7 @@ int launch_fused_cfg(FusedArgs<typename C::R> a, cudaStream_t st) {
   // tensor memory; the TMEM policies size their columns for MINB CTAs/SM
   if constexpr (C::TMX) resident = std::max(resident, C::MINB * num_sms());
   if constexpr (C::HM == H_TEX) {
-    rc = spectra_texture(a.spec, size_t(a.n_fil) * C::VPT * C::T * 16, &a.htex);
+    rc = bind_spectra(a, size_t(a.n_fil) * C::VPT * C::T * 16);
     if (rc) return rc;
   }
   a.fchunk = (g_filter_chunk > 0 && g_filter_chunk < a.n_fil) ? g_filter_chunk
@@ -230,7 +249,7 @@ int launch_w64_cfg(FusedArgs<float> a, cudaStream_t st) {
   if (rc) return rc;
   // TMEM-allocating kernels: the occupancy API reports 1 CTA/SM
   resident = std::max(resident, MINB * num_sms());
-  rc = spectra_texture(a.spec, size_t(a.n_fil) * 1024 * 16, &a.htex);
+  rc = bind_spectra(a, size_t(a.n_fil) * 1024 * 16);
   if (rc) return rc;
   const long long nseg = a.k_hi - a.k_lo;
   const long long warps = (long long)resident * WPC;

@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(WPC * 32, MINB)
   // v = 0..7 at f * 1024 + 128 v + t
   float4 h0[8], h1[8];
   auto fetch = [&](float4* h, int f, int c) {
-    const int base = f * 1024 + 4 * lane + c;
+    const int base = a.hoff + f * 1024 + 4 * lane + c;
 #pragma unroll
     for (int v = 0; v < 8; ++v) h[v] = tex1Dfetch<float4>(a.htex, base + v * 128);
   };

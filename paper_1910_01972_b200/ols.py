@@ -304,10 +304,15 @@ def convolve(signal: Signal, filters: FilterSet, seg_plan: SegmentPlan,
         plain = convolve(signal, filters, seg_plan, variant, None, workers)
         return _derivative(plain, out)
 
-    if variant == "direct_oracle":
-        return _direct(signal, filters, pp)
-    if variant == "full_fft_baseline":
-        return full_fft_convolve(signal, filters, pp)
+    if variant in ("direct_oracle", "full_fft_baseline"):
+        y = (_direct(signal, filters, pp) if variant == "direct_oracle"
+             else full_fft_convolve(signal, filters, pp))
+        if out is None:
+            return y
+        if tuple(out.shape) != tuple(y.shape) or out.dtype != y.dtype:
+            raise ValueError(f"out must be {tuple(y.shape)} {y.dtype}")
+        out.copy_(y)
+        return out
 
     layout = _required_layout(seg_plan.mode, variant)
     if filters.spectra is None:
@@ -478,10 +483,9 @@ def fused_range_launch(x: torch.Tensor, x_base: int, n_s: int,
     streams)."""
     entry = ("olsb_fused_r2r_range" if seg_plan.mode == "r2r"
              else "olsb_fused_c2c_range")
-    if pp.kind not in ("none", "scale") and not (
-            seg_plan.mode == "r2r" and pp.kind == "magnitude_squared"):
-        raise EngineError(f"range launches support postproc none|scale "
-                          f"(r2r: also magnitude_squared), got {pp.kind!r}")
+    if pp.kind not in ("none", "scale", "magnitude_squared"):
+        raise EngineError(f"range launches support postproc none|scale|"
+                          f"magnitude_squared, got {pp.kind!r}")
     _lib.call(entry, x.data_ptr(), x_base, n_s, spec_dev.data_ptr(), n_fil,
               seg_plan.fft_len, seg_plan.tap_len, seg_plan.origin, g_lo, g_hi,
               pp.code, float(pp.scale), out.data_ptr(), out_ld, out_base,

@@ -84,6 +84,10 @@ PP_GRID = [
     (9000, 400, 3, 2048, 0, "r2r", "derivative"),
     (5000, 33, 2, 128, 16, "r2r", "derivative"),
     (1000, 1, 2, 8, 0, "r2r", "derivative"),
+    # complex scale with a factor fp32 cannot represent: the reference
+    # multiplies in float64 and rounds once (_store kind 1)
+    (6000, 65, 3, 512, 32, "c2c", "scale"),
+    (9000, 400, 2, 2048, 0, "c2c", "scale"),
 ]
 
 
@@ -97,7 +101,16 @@ def pp_case_inputs(i):
     return x, taps
 
 
-PP_SCALE = 0.75
+PP_SCALE = 0.75          # r2r scale cells
+PP_SCALE_C2C = 0.3       # c2c scale cells (not representable in fp32)
+
+
+def pp_scale(i):
+    """postproc scale factor of PP_GRID cell i (1.0 unless it is a scale cell)."""
+    mode, ppk = PP_GRID[i][5], PP_GRID[i][6]
+    if ppk != "scale":
+        return 1.0
+    return PP_SCALE if mode == "r2r" else PP_SCALE_C2C
 
 # BASELINE.json configs 1-4 (SURVEY §8 geometry table); cfg5 (2^30) cannot
 # run on the reference and is checked by windows against the oracle instead.

@@ -42,7 +42,7 @@ sys.path.insert(0, "/root/reference/pkg/src")
 import olsconv as oc  # noqa: E402  (the reference)
 
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
-from cases import (CFGS, CONV_GRID, PP_GRID, PP_SCALE, WIN,  # noqa: E402
+from cases import (CFGS, CONV_GRID, PP_GRID, WIN, pp_scale,  # noqa: E402
                    conv_case_inputs, gen_inputs, pp_case_inputs,
                    window_starts)
 from olsconv import Precision  # noqa: E402
@@ -111,7 +111,7 @@ def pp_fixtures():
     for i, (ns, m, nfil, n, origin, mode, ppk) in enumerate(PP_GRID):
         x, taps = pp_case_inputs(i)
         p = oc.plan(ns, m, mode, origin, n)
-        pp = oc.PostProcSpec(ppk, PP_SCALE if ppk == "scale" else 1.0)
+        pp = oc.PostProcSpec(ppk, pp_scale(i))
         vk = "real" if mode == "r2r" else "complex"
         for prec in Precision:
             sig = oc.make_signal(x, vk, prec)

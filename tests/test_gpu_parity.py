@@ -477,6 +477,28 @@ def test_fused_exact_scale_abs2_and_workers(oc):
     assert np.array_equal(a2.cpu().numpy(), want.astype(np.float32))
 
 
+def test_fused_exact_scale_bit_identical_to_reference(oc, golden):
+    """Exact mode with postproc scale 0.3 equals the reference's own fp32 and
+    fp64 outputs (pp_cases.npz, made by the reference) bit for bit: pp_c is
+    applied in float64 and rounded once, as the reference's _store does."""
+    from cases import PP_GRID, pp_case_inputs, pp_scale
+    cells = [i for i, c in enumerate(PP_GRID) if c[5] == "c2c" and c[6] == "scale"]
+    assert cells
+    for i in cells:
+        ns, m, nfil, n, origin, _, _ = PP_GRID[i]
+        x, taps = pp_case_inputs(i)
+        p = oc.plan(ns, m, "c2c", origin, n)
+        for prec in ("single", "double"):
+            P = oc.Precision(prec)
+            y = oc.convolve(oc.make_signal(x, "complex", P),
+                            oc.make_filterset(taps, origin, P), p,
+                            variant="fused_exact",
+                            postproc=oc.PostProcSpec("scale", pp_scale(i)),
+                            workers=2)
+            ref = torch.from_numpy(golden["pp"][f"y_{prec}_{i}"])
+            assert torch.equal(y.cpu(), ref), (i, prec)
+
+
 def test_fused_exact_host_streaming(oc, golden):
     """Exact mode from a pinned host signal into a pinned host output (row
     chunks, contiguous D2H) equals the reference's fp32 output bit for bit."""

@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 import torch
 
-from cases import PP_GRID, PP_SCALE, pp_case_inputs
+from cases import PP_GRID, pp_case_inputs, pp_scale
 from conftest import rel_err, rel_l2_per_filter
 
 pytestmark = pytest.mark.gpu
@@ -33,7 +33,7 @@ def _run(oc, case, prec, out=None, workers=1, layout="natural"):
     P = oc.Precision(prec)
     vk = "real" if mode == "r2r" else "complex"
     p = oc.plan(ns, m, mode, origin, n)
-    pp = oc.PostProcSpec(ppk, PP_SCALE if ppk == "scale" else 1.0)
+    pp = oc.PostProcSpec(ppk, pp_scale(case))
     fs = oc.transform_filters(oc.make_filterset(taps, origin, P), p,
                               "natural" if mode == "r2r" else "permuted")
     return oc.convolve(oc.make_signal(x, vk, P), fs, p, postproc=pp, out=out,
@@ -75,7 +75,7 @@ def test_r2r_splits_bit_identical(oc):
         x, _ = pp_case_inputs(case)
         P = oc.Precision.single
         sig = oc.make_signal(x, "real", P)
-        pp = oc.PostProcSpec(ppk, PP_SCALE if ppk == "scale" else 1.0)
+        pp = oc.PostProcSpec(ppk, pp_scale(case))
         le = p.valid_len
         c = torch.full_like(a, float("nan"))
         cuts = [0, 1, le + 3, 3 * le, 3 * le + 1, ns // 2, ns - 2, ns]
@@ -239,3 +239,51 @@ def test_executor_and_graph_replay_bit_identical(oc, mode, ppk):
     assert torch.equal(out, want)
     with pytest.raises(ValueError):
         ex(sig.samples[:-1])
+
+
+def test_streaming_small_n_filter_chunks(oc):
+    """Host streaming in row chunks whose spectra start at a filter offset
+    that is not texture-aligned (N = 16: 128-byte rows): the engine binds the
+    aligned-down base and offsets its fetches.  Bit-identical to the device
+    path, for c2c, c2c magnitude_squared and r2r."""
+    ns, m, nfil, n = 5000, 9, 7, 16
+    rng = np.random.default_rng([91, ns, nfil])
+    x = rng.standard_normal(ns) + 1j * rng.standard_normal(ns)
+    taps = rng.standard_normal((nfil, m)) + 1j * rng.standard_normal((nfil, m))
+    P = oc.Precision.single
+    for mode, ppk in (("c2c", "none"), ("c2c", "magnitude_squared"),
+                      ("r2r", "none")):
+        xs = x if mode == "c2c" else x.real
+        ts = taps if mode == "c2c" else taps.real
+        vk = "complex" if mode == "c2c" else "real"
+        p = oc.plan(ns, m, mode, 0, n)
+        fs = oc.transform_filters(oc.make_filterset(ts, 0, P), p,
+                                  "permuted" if mode == "c2c" else "natural")
+        pp = oc.PostProcSpec(ppk)
+        dev = oc.convolve(oc.make_signal(xs, vk, P), fs, p, postproc=pp)
+        host = torch.full(tuple(dev.shape), float("nan"),
+                          dtype=dev.dtype).pin_memory()
+        hsig = oc.make_signal(torch.from_numpy(np.ascontiguousarray(xs).astype(
+            np.complex64 if mode == "c2c" else np.float32)).pin_memory(),
+            vk, P, device="cpu")
+        oc.convolve(hsig, fs, p, postproc=pp, out=host)
+        assert torch.equal(host, dev.cpu()), (mode, ppk)
+
+
+def test_comparison_variants_fill_out(oc):
+    """direct_oracle / full_fft_baseline write a caller-provided `out`."""
+    ns, m, nfil, n = 3000, 17, 2, 64
+    rng = np.random.default_rng([92, ns])
+    x = rng.standard_normal(ns) + 1j * rng.standard_normal(ns)
+    taps = rng.standard_normal((nfil, m)) + 1j * rng.standard_normal((nfil, m))
+    P = oc.Precision.single
+    p = oc.plan(ns, m, "c2c", 0, n)
+    sig = oc.make_signal(x, "complex", P)
+    fs = oc.make_filterset(taps, 0, P)
+    for variant in ("direct_oracle", "full_fft_baseline"):
+        out = torch.full((nfil, ns), float("nan"), dtype=torch.complex64,
+                         device="cuda")
+        y = oc.convolve(sig, fs, p, variant=variant, out=out)
+        assert y is out and torch.isfinite(torch.view_as_real(out)).all()
+        ref = oc.convolve(sig, fs, p, variant=variant)
+        assert torch.equal(out, ref)

@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import oracle
-from cases import CONV_GRID, PP_GRID, PP_SCALE, conv_case_inputs, pp_case_inputs
+from cases import CONV_GRID, PP_GRID, conv_case_inputs, pp_case_inputs, pp_scale
 from conftest import rel_err
 
 
@@ -129,7 +129,7 @@ def test_pp_fixtures_match_direct_oracle(golden, case):
     x, taps = pp_case_inputs(case)
     y = oracle.direct_convolve(x, taps, origin)
     if ppk == "scale":
-        y = y * PP_SCALE
+        y = y * pp_scale(case)
     if mode == "r2r":
         y = y.real
         if ppk == "magnitude_squared":
@@ -149,3 +149,17 @@ def test_pp_fixtures_match_direct_oracle(golden, case):
     assert ref.shape == (nfil, ns)
     assert np.isrealobj(ref) == (mode == "r2r" or ppk == "magnitude_squared")
     assert rel_err(ref, y) < 1e-10
+
+
+@pytest.mark.parametrize("case", [i for i, c in enumerate(PP_GRID)
+                                  if c[5] == "c2c" and c[6] == "scale"])
+def test_fused_scale_bit_exact_vs_reference(golden, case):
+    """postproc scale with a factor fp32 cannot represent (0.3): the
+    reference rounds float64(pp_c) x sample once into complex64 (_store kind
+    1, _kernels_nb.py:223-225); the oracle reproduces its fp32 output bit for
+    bit (the GPU exact mode is checked against the same fixtures)."""
+    ns, m, nfil, n, origin, mode, ppk = PP_GRID[case]
+    x, taps = pp_case_inputs(case)
+    y = oracle.fused_convolve(x, taps, n, origin, "single", pp_kind=1,
+                              pp_c=pp_scale(case))
+    assert np.array_equal(y, golden["pp"][f"y_single_{case}"])
