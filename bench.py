@@ -181,6 +181,115 @@ def run_reference(args, rank: int):
     print(json.dumps(line), flush=True)
 
 
+CFG5 = dict(ns=1 << 30, m=512, nfil=64, n=4096)
+CFG5_TILE = 1 << 26      # outputs per filter per pass (64 x 2^26 x 8 B = 32 GiB)
+
+
+def run_cfg5(args, world, rank, dev, ob, emulate):
+    """BASELINE config 5 (north_star's scaling shape): 2^30 complex samples,
+    64 filters M=512, N=4096, halo-sharded over G GPUs (G = the torchrun
+    world, or ``emulate`` ranks run one after another on this GPU).  Each
+    rank holds its contiguous shard in a persistent halo'd buffer
+    (sharding.HaloBuffer) that receives only the (M-1)-sample halos per step
+    (NCCL P2P; device copies when emulated) and produces its 2^30/G x 64
+    outputs in passes of CFG5_TILE outputs per filter into one reused 32 GiB
+    tile (256 GiB per rank at G = 2 does not fit HBM).  Time per rank: CUDA
+    events on the rank's stream around halo exchange + every pass; the job
+    time is the max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_1910_01972_b200.sharding import (HaloBuffer,
+                                                convolve_shard_chunked,
+                                                make_shards)
+    c = CFG5
+    G = emulate or world
+    P = ob.Precision.single
+    p = ob.plan(c["ns"], c["m"], "c2c", 0, c["n"])
+    shards = make_shards(p, G)
+    rng = np.random.default_rng([0, c["ns"], c["m"], c["nfil"], 0, 0])
+    taps = (rng.standard_normal((c["nfil"], c["m"]))
+            + 1j * rng.standard_normal((c["nfil"], c["m"])))
+    fs = ob.transform_filters(ob.make_filterset(taps, 0, P, device=dev), p,
+                              "permuted")
+    spec = fs.spectra_dev
+    own_max = max(s.g_hi - s.g_lo for s in shards)
+    tile = torch.empty((c["nfil"], min(CFG5_TILE, own_max)),
+                       dtype=torch.complex64, device=dev)
+    gen = torch.Generator(device=dev)
+    steps = max(1, min(args.steps, args.cfg5_steps))
+
+    def time_rank(hb, exchange):
+        for _ in range(2):                  # warm-up
+            exchange()
+            convolve_shard_chunked(hb.buffer, hb.shard, p, spec, c["nfil"], P,
+                                   tile)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        passes = 0
+        for _ in range(steps):
+            exchange()
+            passes = convolve_shard_chunked(hb.buffer, hb.shard, p, spec,
+                                            c["nfil"], P, tile)
+        e1.record()
+        e1.synchronize()
+        return e0.elapsed_time(e1) / steps, passes
+
+    per_rank = []
+    if emulate:
+        # one global signal; every emulated rank copies its shard into its
+        # own halo'd buffer (untimed), then times halo copies + its passes
+        xg = torch.randn(c["ns"], dtype=torch.complex64, device=dev,
+                         generator=gen.manual_seed(0))
+        for r in range(G):
+            hb = HaloBuffer(shards, r, torch.complex64, dev)
+            sh = shards[r]
+            hb.own.copy_(xg[sh.g_lo:sh.g_hi])
+            ms, passes = time_rank(hb, lambda hb=hb: hb.fill_from(xg))
+            per_rank.append((ms, sh.g_hi - sh.g_lo, passes, hb.halo_samples))
+            del hb
+        del xg
+    else:
+        hb = HaloBuffer(shards, rank, torch.complex64, dev)
+        sh = shards[rank]
+        hb.own.copy_(torch.randn(sh.g_hi - sh.g_lo, dtype=torch.complex64,
+                                 device=dev, generator=gen.manual_seed(rank)))
+        ms, passes = time_rank(hb, hb.exchange if world > 1 else (lambda: None))
+        mine = torch.tensor([ms, sh.g_hi - sh.g_lo, passes, hb.halo_samples],
+                            dtype=torch.float64, device=dev)
+        if world > 1:
+            allv = [torch.empty_like(mine) for _ in range(world)]
+            dist.all_gather(allv, mine)
+            per_rank = [tuple(v.tolist()) for v in allv]
+        else:
+            per_rank = [tuple(mine.tolist())]
+    del tile
+    torch.cuda.empty_cache()
+    hbm, _ = peaks()
+    t_max = max(r[0] for r in per_rank)
+    fracs = [8 * r[1] * (1 + c["nfil"]) / (r[0] * 1e-3) / 1e9 / hbm
+             for r in per_rank]
+    return {
+        "workload": "cfg5: 2^30 complex fp32 samples, 64 filters M=512, "
+                    f"N=4096, halo-sharded over {G} GPU(s)",
+        "gpus": G, "emulated": bool(emulate),
+        "value": c["ns"] * c["nfil"] / (t_max * 1e-3), "unit": "samples/s",
+        "ms_per_step": t_max,
+        "per_rank_ms": [round(r[0], 3) for r in per_rank],
+        "per_gpu_hbm_frac": [round(f, 4) for f in fracs],
+        "passes_per_rank": int(max(r[2] for r in per_rank)),
+        "halo_samples_per_rank": [int(r[3]) for r in per_rank],
+        "steps": steps,
+        "note": ("ranks run one after another on one GPU; halos are device "
+                 "copies; value = outputs of all ranks / max rank time"
+                 if emulate else
+                 "one process per GPU; halos by NCCL P2P; max over ranks"),
+    }
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -191,6 +300,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-cufft", action="store_true")
+    ap.add_argument("--no-cfg5", action="store_true")
+    ap.add_argument("--cfg5-steps", type=int, default=3)
+    ap.add_argument("--emulate-ranks", type=int, default=0,
+                    help="cfg5 leg only: emulate G ranks on this one GPU")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -206,7 +319,9 @@ def main():
     import torch.distributed as dist
     import paper_1910_01972_b200 as ob
     from paper_1910_01972_b200.ols import fused_range_launch
-    from paper_1910_01972_b200.sharding import exchange_halos, make_shards
+    from paper_1910_01972_b200.sharding import (HaloBuffer,
+                                                convolve_shard_chunked,
+                                                make_shards)
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -230,20 +345,22 @@ def main():
         x_np = rng.standard_normal(n_own) + 1j * rng.standard_normal(n_own)
         taps = (np.random.default_rng([0, ns_global, M, NFIL, 0, 0])
                 .standard_normal((NFIL, M)) * (1 + 1j))
-    own = torch.from_numpy(x_np[me.g_lo:me.g_hi] if world == 1 else x_np).to(
-        dev, torch.complex64)
+    # the rank's persistent halo'd input: owned samples written once, only
+    # the (M-1) halo samples move per step (NCCL P2P)
+    hb = HaloBuffer(shards, rank, torch.complex64, dev)
+    hb.own.copy_(torch.from_numpy(x_np[me.g_lo:me.g_hi] if world == 1
+                                  else x_np).to(dev, torch.complex64))
     fs = ob.transform_filters(ob.make_filterset(taps, 0, P, device=dev), p,
                               "permuted")
     out = torch.empty((NFIL, n_own), dtype=torch.complex64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     def step(ev=None):
-        xl = exchange_halos(own, shards, rank) if world > 1 else own
+        xl = hb.exchange() if world > 1 else hb.buffer
         if ev is not None:
             ev[0].record()
-        fused_range_launch(xl, me.x_lo if world > 1 else me.g_lo, ns_global,
-                           fs.spectra_dev, NFIL, p, me.g_lo, me.g_hi, ob.NONE,
-                           out, n_own, me.g_lo, P)
+        fused_range_launch(xl, me.x_lo, ns_global, fs.spectra_dev, NFIL, p,
+                           me.g_lo, me.g_hi, ob.NONE, out, n_own, me.g_lo, P)
         if ev is not None:
             ev[1].record()
 
@@ -283,16 +400,20 @@ def main():
     kmean = statistics.mean(kern_ms)
     alg_bytes = 8 * n_own * (1 + NFIL)
     achieved = alg_bytes / (kmean * 1e-3) / 1e9
-    traffic = None
+    traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", "traffic_cfg3.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and world == 1:
         with open(tpath) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
+            tj = json.load(f)
+        traffic = tj.get("dram_bytes_per_launch")
+        traffic_src = ("ncu --set full dram__bytes_read.sum + "
+                       "dram__bytes_write.sum of the same kernel, from "
+                       f"profiles/traffic_cfg3.json ({tj.get('source', '')})"
+                       " -- not measured in this run")
 
     # ---- end to end through the public API from pinned host memory
     e2e = None
     if not args.no_e2e:
-        xh_lo, xh_hi = me.x_lo, me.x_hi
         if world == 1:
             xh = torch.from_numpy(x_np.astype(np.complex64)).pin_memory()
             hsig = ob.make_signal(xh, "complex", P, device="cpu")
@@ -309,48 +430,55 @@ def main():
             e1.synchronize()
             e_ms = e0.elapsed_time(e1) / args.e2e_steps
             h2d = xh.numel() * 8
+            path = ("make_signal(pinned host) + convolve(out=pinned host) "
+                    "streaming row chunks (contiguous D2H)")
         else:
-            # every rank streams its own shard (owned samples + halos)
-            own_h = torch.empty(xh_hi - xh_lo, dtype=torch.complex64)
-            own_h[me.g_lo - xh_lo:me.g_hi - xh_lo] = own.cpu()
-            xl = exchange_halos(own, shards, rank).cpu()
-            own_h.copy_(xl)
-            xh = own_h.pin_memory()
+            # every rank: its owned samples from pinned host memory into its
+            # halo'd buffer, halo exchange, its outputs in passes, each pass
+            # copied to pinned host memory (sharding module's public API)
+            own_h = torch.from_numpy(x_np.astype(np.complex64)).pin_memory()
             hout = torch.empty((NFIL, n_own), dtype=torch.complex64).pin_memory()
-            from paper_1910_01972_b200.ols import _lib  # noqa: F401
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            xd = torch.empty_like(xh, device=dev)
+            tile_w = max(1, min(n_own, (256 << 20) // (8 * NFIL)))
+            tile = torch.empty((NFIL, tile_w), dtype=torch.complex64, device=dev)
+
+            def sink(g_a, g_b, t):
+                hout[:, g_a - me.g_lo:g_b - me.g_lo].copy_(
+                    t[:, :g_b - g_a], non_blocking=True)
+
+            def e2e_step():
+                hb.own.copy_(own_h, non_blocking=True)
+                hb.exchange()
+                convolve_shard_chunked(hb.buffer, me, p, fs.spectra_dev, NFIL,
+                                       P, tile, sink)
+
+            e2e_step()
             torch.cuda.synchronize()
             dist.barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
             for _ in range(args.e2e_steps):
-                xd.copy_(xh, non_blocking=True)
-                fused_range_launch(xd, xh_lo, ns_global, fs.spectra_dev, NFIL,
-                                   p, me.g_lo, me.g_hi, ob.NONE, out, n_own,
-                                   me.g_lo, P)
-                hout.copy_(out, non_blocking=True)
+                e2e_step()
             e1.record()
             e1.synchronize()
             e_ms = e0.elapsed_time(e1) / args.e2e_steps
-            h2d = xh.numel() * 8
+            h2d = own_h.numel() * 8
+            path = ("per rank: pinned shard -> HaloBuffer.own, NCCL halo "
+                    "exchange, convolve_shard_chunked with a D2H sink per pass")
         te = torch.tensor([e_ms], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": outputs_per_step / (float(te.item()) * 1e-3),
                "unit": "samples/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(NFIL * n_own * 8),
-               "ms_per_step": float(te.item()),
-               "path": "make_signal(pinned host) + convolve(out=pinned host)"
-                       " streaming row chunks (contiguous D2H)" if world == 1 else
-                       "per-rank H2D shard + fused_range + D2H"}
+               "ms_per_step": float(te.item()), "path": path}
 
     # ---- the paper's comparison point: cuFFT-based OLS (Algorithm 1,
     # convolve(variant="pipelined")) on the same shard, same N
     cufft = None
     if not args.no_cufft:
         pc = ob.plan(n_own, M, "c2c", 0, NFFT)
-        sig_own = ob.make_signal(own, "complex", P)
+        sig_own = ob.make_signal(hb.own, "complex", P)
         fc = ob.transform_filters(ob.make_filterset(taps, 0, P, device=dev),
                                   pc, "natural")
         ob.convolve(sig_own, fc, pc, variant="pipelined", out=out)
@@ -374,7 +502,7 @@ def main():
     # same shard and grid, device-resident, one launch per step
     exact = None
     if world == 1 and not args.no_cufft:
-        sig1 = ob.make_signal(own, "complex", P)
+        sig1 = ob.make_signal(hb.own, "complex", P)
         fs1 = ob.make_filterset(taps, 0, P, device=dev)
         ob.convolve(sig1, fs1, p, variant="fused_exact", out=out)
         torch.cuda.synchronize()
@@ -394,6 +522,14 @@ def main():
                          "the reference's fp32 fused_c2c (includes the exact "
                          "filter-spectra transform per call)"}
 
+    # ---- BASELINE config 5 (the scaling shape), after the cfg3 buffers go
+    cfg5 = None
+    if not args.no_cfg5:
+        del out, flush
+        torch.cuda.empty_cache()
+        cfg5 = run_cfg5(args, world, rank, dev, ob,
+                        args.emulate_ranks if world == 1 else 0)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
@@ -412,12 +548,14 @@ def main():
             "config": {"workload": WORKLOAD, "signal_samples": ns_global,
                        "filters": NFIL, "taps": M, "fft_len": NFFT,
                        "parallelism": f"signal sharded over {world} GPU(s), "
-                                      "halo exchange by NCCL P2P",
+                                      "persistent halo'd buffers, halo "
+                                      "exchange by NCCL P2P",
                        "l2": "flushed between timed steps (256 MiB memset)"},
             "hbm_frac": achieved / hbm,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm,
                          "unit": "GB/s", "frac": achieved / hbm,
-                         "traffic": traffic, "peak_source": peak_kind,
+                         "traffic": traffic, "traffic_source": traffic_src,
+                         "peak_source": peak_kind,
                          "alg_bytes_per_launch": alg_bytes,
                          "kernel_ms": kmean},
             "cpu_baseline": cpu,
@@ -425,6 +563,7 @@ def main():
             "gpu_launches": args.steps,
             "cufft_ols": cufft,
             "exact_mode": exact,
+            "cfg5": cfg5,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

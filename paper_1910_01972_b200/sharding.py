@@ -111,6 +111,93 @@ def exchange_halos(own: torch.Tensor, shards: List[Shard], rank: int,
     return buf
 
 
+class HaloBuffer:
+    """Persistent halo'd input of one rank: ``buffer`` holds input samples
+    [x_lo, x_hi); the rank writes its owned samples into ``own`` (the view
+    [g_lo, g_hi)) once, and every step :meth:`exchange` moves ONLY the halos
+    -- the (M-1-o) samples left and o right of the shard, each from the
+    neighbour that owns them -- by one batched NCCL send/recv (NVLink P2P on
+    B200; gloo on CPU).  No allocation and no copy of the owned range per
+    step, no collective.
+    """
+
+    def __init__(self, shards: List[Shard], rank: int, dtype, device,
+                 group=None):
+        self.shards = shards
+        self.rank = rank
+        self.group = group
+        me = shards[rank]
+        self.shard = me
+        self.buffer = torch.zeros(max(1, me.x_hi - me.x_lo), dtype=dtype,
+                                  device=device)
+        self.own = self.buffer[me.g_lo - me.x_lo:me.g_hi - me.x_lo]
+        # (peer, recv view of my buffer) / (peer, send view of my own range)
+        self.recvs, self.sends = [], []
+        for peer in shards:
+            if peer.rank == rank:
+                continue
+            lo, hi = max(me.x_lo, peer.g_lo), min(me.x_hi, peer.g_hi)
+            if hi > lo:
+                self.recvs.append((peer.rank,
+                                   self.buffer[lo - me.x_lo:hi - me.x_lo]))
+            lo, hi = max(peer.x_lo, me.g_lo), min(peer.x_hi, me.g_hi)
+            if hi > lo:
+                self.sends.append((peer.rank,
+                                   self.buffer[lo - me.x_lo:hi - me.x_lo]))
+
+    @property
+    def halo_samples(self) -> int:
+        return sum(v.numel() for _, v in self.recvs)
+
+    def exchange(self) -> torch.Tensor:
+        """Receive this step's halos (the neighbours' boundary samples) into
+        the buffer; returns the buffer ([x_lo, x_hi))."""
+        ops = [dist.P2POp(dist.irecv, v, peer, self.group)
+               for peer, v in self.recvs]
+        ops += [dist.P2POp(dist.isend, v, peer, self.group)
+                for peer, v in self.sends]
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        return self.buffer
+
+    def fill_from(self, x_global: torch.Tensor) -> torch.Tensor:
+        """Single-process emulation of :meth:`exchange` (one GPU standing in
+        for several ranks): the halos are device copies out of the global
+        signal instead of P2P receives."""
+        for peer, v in self.recvs:
+            off = self.shard.x_lo + (v.data_ptr() - self.buffer.data_ptr()) // v.element_size()
+            v.copy_(x_global[off:off + v.numel()])
+        return self.buffer
+
+
+def convolve_shard_chunked(x_local: torch.Tensor, shard: Shard,
+                           seg_plan: SegmentPlan, spec_dev: torch.Tensor,
+                           n_fil: int, precision, out_chunk: torch.Tensor,
+                           sink=None, stream: Optional[int] = None) -> int:
+    """This rank's outputs [g_lo, g_hi) in passes of ``out_chunk.shape[1]``
+    outputs per filter into the reused device tile ``out_chunk`` (n_fil x
+    w): the per-rank output can exceed HBM (cfg5 at 2 GPUs: 256 GiB per
+    rank).  ``sink(g_a, g_b, tile)`` consumes each pass (copy out, reduce,
+    or nothing when only the device throughput is measured).  Pass
+    boundaries are multiples of the engine's segment grid only for
+    efficiency; any cut is bit-identical (the grid is anchored at sample 0).
+    Returns the number of launches."""
+    from .postproc import NONE
+    from .ols import fused_range_launch
+    w = out_chunk.shape[1]
+    launches = 0
+    for g_a in range(shard.g_lo, shard.g_hi, w):
+        g_b = min(g_a + w, shard.g_hi)
+        fused_range_launch(x_local, shard.x_lo, seg_plan.signal_len, spec_dev,
+                           n_fil, seg_plan, g_a, g_b, NONE, out_chunk, w, g_a,
+                           precision, stream)
+        launches += 1
+        if sink is not None:
+            sink(g_a, g_b, out_chunk)
+    return launches
+
+
 def convolve_shard(x_local: torch.Tensor, shard: Shard, seg_plan: SegmentPlan,
                    filters, out: Optional[torch.Tensor] = None,
                    postproc=None) -> torch.Tensor:

@@ -396,6 +396,51 @@ def test_cfg5_geometry_windows_vs_oracle(oc):
         assert rel_l2_per_filter(out.cpu().numpy(), ref) <= L2_TOL, a
 
 
+def test_cfg5_shard_seams_from_halo_buffers(oc):
+    """cfg5 sharded over G = 2, 4, 8 ranks: every rank's persistent halo'd
+    buffer (sharding.HaloBuffer, halos filled as the transport would) alone
+    produces the outputs at both ends of its shard -- through the chunked
+    shard engine (convolve_shard_chunked) -- bit-identical to the unsharded
+    launch over the global signal and within the fp32 bar of the oracle."""
+    from paper_1910_01972_b200.ols import fused_range_launch
+    from paper_1910_01972_b200.sharding import (HaloBuffer,
+                                                convolve_shard_chunked,
+                                                make_shards)
+    ns, m, nfil, n = 1 << 30, 512, 64, 4096
+    gen = torch.Generator(device="cuda").manual_seed(1)
+    xs = torch.randn(ns, dtype=torch.complex64, device="cuda", generator=gen)
+    rng = np.random.default_rng([0, ns, m, nfil, 0, 0])
+    taps = rng.standard_normal((4, m)) + 1j * rng.standard_normal((4, m))
+    P = oc.Precision.single
+    p = oc.plan(ns, m, "c2c", 0, n)
+    fs = oc.transform_filters(oc.make_filterset(taps, 0, P), p, "permuted")
+    w = 300
+    tile = torch.empty((4, w), dtype=torch.complex64, device="cuda")
+    for world in (2, 4, 8):
+        shards = make_shards(p, world)
+        for r, sh in enumerate(shards):
+            hb = HaloBuffer(shards, r, torch.complex64, "cuda")
+            hb.own.copy_(xs[sh.g_lo:sh.g_hi])
+            hb.fill_from(xs)
+            for a in (sh.g_lo, sh.g_hi - w):
+                seg = type(sh)(sh.rank, sh.world, a, a + w, sh.x_lo, sh.x_hi)
+                got = {}
+                convolve_shard_chunked(
+                    hb.buffer, seg, p, fs.spectra_dev, 4, P, tile,
+                    sink=lambda ga, gb, t: got.setdefault(ga, t.clone()))
+                want = torch.empty((4, w), dtype=torch.complex64, device="cuda")
+                fused_range_launch(xs, 0, ns, fs.spectra_dev, 4, p, a, a + w,
+                                   oc.NONE, want, w, a, P)
+                assert torch.equal(got[a], want), (world, r, a)
+                lo = max(0, a - (m - 1))
+                xw = xs[lo:a + w].cpu().numpy().astype(np.complex128)
+                full = np.zeros(a + w - (a - (m - 1)), np.complex128)
+                full[lo - (a - (m - 1)):] = xw
+                ref = oracle.direct_window(full, taps, 0, m - 1, m - 1 + w)
+                assert rel_l2_per_filter(got[a].cpu().numpy(), ref) <= L2_TOL
+            del hb
+
+
 @pytest.mark.parametrize("mode", ["c2c", "r2r"])
 def test_beyond_int32_sample_indices_vs_oracle(oc, mode):
     """N_s = 2^31 + 12345 samples (c2c: 17 GB in, 17 GB out): every sample

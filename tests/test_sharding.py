@@ -12,7 +12,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import paper_1910_01972_b200 as oc
-from paper_1910_01972_b200.sharding import exchange_halos, make_shards
+from paper_1910_01972_b200.sharding import (HaloBuffer, exchange_halos,
+                                            make_shards)
 
 
 def _free_port():
@@ -99,3 +100,51 @@ def test_gloo_halo_exchange(world, case):
         ok_buf, err = ret[r]
         assert ok_buf, r
         assert err == 0.0, (r, err)
+
+
+def _worker_halo_buffer(rank, world, port, case, ret):
+    """Persistent halo'd buffer: owned samples written once, every step moves
+    only the halos.  Two steps with new owned data; after each exchange the
+    buffer equals the global signal over [x_lo, x_hi)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ns, m, nfil, n, origin = case
+        p = oc.plan(ns, m, "c2c", origin, n)
+        shards = make_shards(p, world)
+        me = shards[rank]
+        hb = HaloBuffer(shards, rank, torch.complex128, "cpu")
+        ok = []
+        moved = hb.halo_samples
+        for step in range(2):
+            rng = np.random.default_rng([8, step, ns, m])
+            x = rng.standard_normal(ns) + 1j * rng.standard_normal(ns)
+            hb.own.copy_(torch.from_numpy(x[me.g_lo:me.g_hi]))
+            buf = hb.exchange()
+            ok.append(np.array_equal(buf.numpy()[:me.x_hi - me.x_lo],
+                                     x[me.x_lo:me.x_hi]))
+        ret[rank] = (all(ok), moved, (me.g_lo - me.x_lo) + (me.x_hi - me.g_hi))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("case", range(len(CASES)))
+def test_gloo_persistent_halo_buffer(world, case):
+    ctx = mp.get_context("spawn")
+    mgr = ctx.Manager()
+    ret = mgr.dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_halo_buffer,
+                         args=(r, world, port, CASES[case], ret))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(120)
+        assert pr.exitcode == 0
+    for r in range(world):
+        ok, moved, halo = ret[r]
+        assert ok, r
+        assert moved == halo, (r, moved, halo)   # only the halos move
