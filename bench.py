@@ -493,10 +493,33 @@ def main():
             e1.synchronize()
             c_ms.append(e0.elapsed_time(e1))
         cm = statistics.median(c_ms)
-        cufft = {"ms_per_step": cm, "value": n_own * NFIL / (cm * 1e-3) * world,
-                 "unit": "samples/s", "speedup_fused": cm / kmean,
-                 "path": "gather -> batched C2C cuFFT -> multiply -> batched "
-                         "inverse C2C -> discard (chunked), same N"}
+        # the paper's comparison point in its fastest form here: per L2-sized
+        # chunk, batched C2C over the overlapping windows (no gather),
+        # multiply kernel, batched inverse, discard kernel
+        ob.convolve(sig_own, fc, pc, variant="cufft_ols", out=out)
+        torch.cuda.synchronize()
+        k_ms = []
+        for _ in range(5):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            ob.convolve(sig_own, fc, pc, variant="cufft_ols", out=out)
+            e1.record()
+            e1.synchronize()
+            k_ms.append(e0.elapsed_time(e1))
+        km = statistics.median(k_ms)
+        cufft = {"ms_per_step": km, "value": n_own * NFIL / (km * 1e-3) * world,
+                 "unit": "samples/s", "speedup_fused": km / kmean,
+                 "path": "convolve(variant='cufft_ols'), PAPER.md Algorithm "
+                         "1 on L2-resident chunks: batched C2C over the "
+                         "overlapping windows (idist = L), multiply kernel, "
+                         "batched inverse C2C, discard kernel; same N (cuFFT "
+                         "callbacks are not applied on this platform: "
+                         "profiles/r02_cufft_callbacks.log)",
+                 "eager": {"ms_per_step": cm, "speedup_fused": cm / kmean,
+                           "path": "gather -> batched C2C cuFFT -> "
+                                   "materialized multiply -> batched inverse "
+                                   "C2C -> discard (chunked), same N"}}
 
     # the exact mode (the reference's arithmetic, bit-identical outputs) on the
     # same shard and grid, device-resident, one launch per step

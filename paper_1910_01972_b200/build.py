@@ -86,9 +86,29 @@ def build(verbose: bool = False, force: bool = False) -> str:
     return LIB
 
 
+CUFFT_SRC = os.path.join(CSRC, "olsb_cufft.cu")
+CUFFT_LIB = os.path.join(PKG, "libolsb_cufft.so")
+
+
+def build_cufft(force: bool = False) -> str:
+    """libolsb_cufft.so: the paper's cuFFT-OLS comparison point
+    (csrc/olsb_cufft.cu), linked against the dynamic libcufft so the
+    process's already-loaded cuFFT (torch's) is reused."""
+    if (not force and os.path.exists(CUFFT_LIB)
+            and os.path.getmtime(CUFFT_LIB) >= os.path.getmtime(CUFFT_SRC)):
+        return CUFFT_LIB
+    cudalib = os.path.join(os.path.dirname(os.path.dirname(nvcc())), "lib64")
+    _run([nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-shared", CUFFT_SRC,
+          "-o", CUFFT_LIB + ".tmp", "-L", cudalib, "-lcufft",
+          "-Xlinker", f"-rpath={cudalib}"], False)
+    os.replace(CUFFT_LIB + ".tmp", CUFFT_LIB)
+    return CUFFT_LIB
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--verbose", action="store_true")
     ap.add_argument("--force", action="store_true")
     args = ap.parse_args()
     print(build(verbose=args.verbose, force=args.force))
+    print(build_cufft(force=args.force))

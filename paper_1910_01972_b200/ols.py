@@ -40,7 +40,7 @@ from .postproc import NONE, PostProcSpec
 
 MODES = ("c2c", "r2r")
 ENGINE_VARIANTS = ("fused", "pipelined", "full_fft_baseline", "direct_oracle",
-                   "fused_exact")
+                   "fused_exact", "cufft_ols")
 
 DEFAULT_MAX_FULL_LEN = 1 << 25
 PIPELINED_DEFAULT_SEGMENT = 8192
@@ -185,15 +185,24 @@ def transform_filters(filters: FilterSet, seg_plan: SegmentPlan,
             raise PlanMismatch("complex filter taps on the real path")
         if layout != "natural":
             raise LayoutMismatch("packed real spectra are natural-order only")
-        padded = torch.zeros((filters.n_filters, n), dtype=precision.torch_real,
-                             device=taps.device)
-        padded[:, :filters.tap_length] = taps
-        spectra = torch.fft.rfft(padded, dim=1)
-        # the fused real engine transforms two real segments as one complex
-        # one, so it multiplies by the full complex spectrum of the real taps
-        # (engine layout, same in-register FFT as the c2c path); built on
-        # first use by _engine_spectra (segment lengths the engine supports)
-        return filters.with_spectra(spectra, layout, n)
+        # the engine's own in-register FFT of the real taps (zero imaginary
+        # parts): the full complex spectrum, permuted + engine layout.  The
+        # fused real engine multiplies by it (it transforms two real
+        # segments as one complex segment); the host-visible spectra keep
+        # the reference's packed rfft semantics (n/2 + 1 bins, natural
+        # order, ols.py:183-193), read out of the permuted spectrum (bin k
+        # sits at bit-reversed position rev(k))
+        ctaps = taps.to(precision.torch_complex).contiguous()
+        perm = torch.empty((filters.n_filters, n), dtype=precision.torch_complex,
+                           device=taps.device)
+        dev = torch.empty_like(perm)
+        with torch.cuda.device(taps.device):
+            _lib.call("olsb_filter_spectra_c2c", ctaps.data_ptr(),
+                      filters.n_filters, filters.tap_length, n,
+                      perm.data_ptr(), dev.data_ptr(), precision.code,
+                      _stream_ptr())
+        bins = perm[:, _bitrev_index(n, taps.device)[:n // 2 + 1]].contiguous()
+        return filters.with_spectra(bins, layout, n, dev)
     ctaps = taps.to(precision.torch_complex).contiguous()
     if layout == "permuted":
         spectra = torch.empty((filters.n_filters, n),
@@ -209,6 +218,24 @@ def transform_filters(filters: FilterSet, seg_plan: SegmentPlan,
                          device=taps.device)
     padded[:, :filters.tap_length] = ctaps
     return filters.with_spectra(torch.fft.fft(padded, dim=1), layout, n)
+
+
+_BITREV = {}
+
+
+def _bitrev_index(n: int, device) -> torch.Tensor:
+    """rev(k) for k < n (log2 n bits): natural bin k of a permuted spectrum."""
+    key = (n, str(device))
+    t = _BITREV.get(key)
+    if t is None:
+        bits = n.bit_length() - 1
+        k = torch.arange(n)
+        r = torch.zeros(n, dtype=torch.int64)
+        for b in range(bits):
+            r |= ((k >> b) & 1) << (bits - 1 - b)
+        t = r.to(device)
+        _BITREV[key] = t
+    return t
 
 
 def _engine_spectra(filters: FilterSet) -> torch.Tensor:
@@ -372,6 +399,9 @@ def convolve(signal: Signal, filters: FilterSet, seg_plan: SegmentPlan,
     if variant == "fused_exact":
         return _fused_exact(signal, filters, seg_plan, pp, precision, l_eff,
                             t0, win_off, n_seg_eff, out, out_dtype, workers)
+    if variant == "cufft_ols":
+        return _cufft_ols(signal, filters, seg_plan, pp, precision,
+                                    out)
     return _pipelined(signal, filters, seg_plan, pp, precision, l_eff, t0,
                       win_off, n_seg_eff, out)
 
@@ -677,6 +707,35 @@ def _pipelined(signal, filters, seg_plan, pp, precision, l_eff, t0, win_off,
             seg_out = (seg_out * seg_out if real else
                        seg_out.real * seg_out.real + seg_out.imag * seg_out.imag)
         out[:, g_lo:g_hi] = seg_out
+    return out
+
+
+def _cufft_ols(signal, filters, seg_plan, pp, precision, out):
+    """The paper's cuFFT-OLS in its efficient form (PAPER.md Algorithm 1;
+    libolsb_cufft.so, csrc/olsb_cufft.cu): per L2-sized chunk of segments a
+    batched forward C2C that reads the overlapping windows in place (idist =
+    L), then per chunk of filters a multiply kernel, one batched inverse C2C
+    and a store kernel that keeps only the valid samples.  (The paper puts
+    the multiply and the discard into cuFFT callbacks; on this platform
+    cuFFT does not apply them, see csrc/olsb_cufft.cu.)  c2c, single
+    precision, postproc none / scale."""
+    from . import _lib_cufft
+    if (seg_plan.mode != "c2c" or precision != Precision.single
+            or pp.kind not in ("none", "scale")):
+        raise EngineError("variant 'cufft_ols' covers c2c, single "
+                          "precision, postproc none | scale")
+    x = signal.samples
+    if not x.is_cuda:
+        raise ValueError("variant 'cufft_ols' needs a device signal")
+    n, n_s, n_fil = seg_plan.fft_len, signal.length, filters.n_filters
+    if out is None:
+        out = torch.empty((n_fil, n_s), dtype=torch.complex64, device=x.device)
+    spec = filters.spectra.to(device=x.device, dtype=torch.complex64).contiguous()
+    with torch.cuda.device(x.device):
+        _lib_cufft.ols_c2c(x, n_s, spec, n_fil, n, seg_plan.tap_len,
+                           seg_plan.origin, out, n_s, _stream_ptr())
+    if pp.kind == "scale":
+        out.mul_(pp.scale)
     return out
 
 

@@ -294,6 +294,37 @@ def test_variants_agree(oc):
                        fused) < 1e-10, v
 
 
+def test_cufft_callback_ols_vs_reference(oc, golden):
+    """variant="cufft_ols" (the paper's cuFFT-based OLS comparison point:
+    batched C2C over overlapping windows, multiply kernel, batched inverse,
+    discard kernel, on L2-sized chunks) on every c2c golden cell: within the
+    fp32 bar of the reference's float64 result; also the cfg3 shape at a
+    larger size (several segment chunks), and scale."""
+    g = golden["conv"]
+    P = oc.Precision.single
+    for i, (ns, m, nfil, n, origin, real_taps) in enumerate(CONV_GRID):
+        x, taps = conv_case_inputs(i)
+        p = oc.plan(ns, m, "c2c", origin, n)
+        out = torch.full((nfil, ns), float("nan"), dtype=torch.complex64,
+                         device="cuda")
+        y = oc.convolve(oc.make_signal(x, "complex", P),
+                        oc.make_filterset(taps, origin, P), p,
+                        variant="cufft_ols", out=out).cpu().numpy()
+        assert np.all(np.isfinite(y)), i        # every output written once
+        assert rel_l2_per_filter(y, g[f"y_double_{i}"]) <= L2_TOL, i
+    ns, m, nfil, n = 300_000, 400, 4, 2048
+    rng = np.random.default_rng([98, ns])
+    x = rng.standard_normal(ns) + 1j * rng.standard_normal(ns)
+    taps = rng.standard_normal((nfil, m)) + 1j * rng.standard_normal((nfil, m))
+    p = oc.plan(ns, m, "c2c", 0, n)
+    y = oc.convolve(oc.make_signal(x, "complex", P),
+                    oc.make_filterset(taps, 0, P), p,
+                    variant="cufft_ols",
+                    postproc=oc.PostProcSpec("scale", 0.5)).cpu().numpy()
+    ref = 0.5 * oracle.direct_convolve(x, taps, 0)
+    assert rel_l2_per_filter(y, ref) <= L2_TOL
+
+
 def test_error_detection(oc):
     # reference test_ols.py:189-221
     rng = np.random.default_rng(36)

@@ -287,3 +287,20 @@ def test_comparison_variants_fill_out(oc):
         assert y is out and torch.isfinite(torch.view_as_real(out)).all()
         ref = oc.convolve(sig, fs, p, variant=variant)
         assert torch.equal(out, ref)
+
+
+def test_r2r_spectra_from_engine_fft(oc):
+    """transform_filters on the real path: the packed rfft bins (n/2 + 1,
+    natural order, the reference's semantics, ols.py:183-193) come out of
+    the engine's own FFT (no cuFFT), together with the engine layout."""
+    rng = np.random.default_rng([99])
+    for n, m in ((8, 3), (1024, 257), (4096, 1025)):
+        taps = rng.standard_normal((3, m))
+        p = oc.plan(10_000, m, "r2r", 0, n)
+        fs = oc.transform_filters(oc.make_filterset(taps, 0, oc.Precision.single),
+                                  p, "natural")
+        assert fs.spectra.shape == (3, n // 2 + 1) and fs.spectra_dev is not None
+        padded = np.zeros((3, n))
+        padded[:, :m] = taps
+        want = np.fft.rfft(padded, axis=1)
+        assert rel_l2_per_filter(fs.spectra.cpu().numpy(), want) <= 1e-6, n

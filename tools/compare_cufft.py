@@ -78,6 +78,16 @@ def run(name):
             best = (nc, t)
         if nc == n:
             res["speedup_same_n"] = t / t_fused
+    if mode == "c2c" and n <= 4096:
+        # the L2-chunked cuFFT OLS (libolsb_cufft.so): no gather copy,
+        # product chunks stay in L2
+        fn = ob.transform_filters(fset, p, "natural")
+        t = timed(lambda: ob.convolve(sig, fn, p, variant="cufft_ols",
+                                      out=out), reps=5, warm=2)
+        res["cufft_l2_ms"] = t * 1e3
+        res["cufft_l2_maxrel_vs_fused"] = float(
+            (out - ref).abs().max() / ref.abs().max())
+        res["speedup_vs_cufft_l2"] = t / t_fused
     res["cufft_best_n"] = best[0]
     res["speedup_vs_cufft_best"] = best[1] / t_fused
     return res
