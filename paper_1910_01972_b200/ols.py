@@ -192,6 +192,13 @@ def transform_filters(filters: FilterSet, seg_plan: SegmentPlan,
         # the reference's packed rfft semantics (n/2 + 1 bins, natural
         # order, ols.py:183-193), read out of the permuted spectrum (bin k
         # sits at bit-reversed position rev(k))
+        if n > 4096:
+            # segment lengths beyond the engine's (the cuFFT comparison path
+            # only): cuFFT's rfft
+            padded = torch.zeros((filters.n_filters, n),
+                                 dtype=precision.torch_real, device=taps.device)
+            padded[:, :filters.tap_length] = taps
+            return filters.with_spectra(torch.fft.rfft(padded, dim=1), layout, n)
         ctaps = taps.to(precision.torch_complex).contiguous()
         perm = torch.empty((filters.n_filters, n), dtype=precision.torch_complex,
                            device=taps.device)
