@@ -766,6 +766,60 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     }
   };
 
+  // L2 prefetch (TMA, one thread) of item `itn`'s input window: the live
+  // segments of its group only, so it stays inside the input extent the
+  // caller guarantees for [k_lo, k_hi)
+  auto prefetch_window = [&](long long itn) {
+    long long gn = itn / nfch;
+    if constexpr (TS) {
+      int fn_, wn_;
+      item(itn, gn, fn_, wn_);
+    }
+    const long long sn = a.k_lo + gn * C::SEGS;
+    const long long nl = a.k_hi - sn < C::SEGS ? a.k_hi - sn : C::SEGS;
+    const long long segs = MODE == FMODE_R2R ? 2 * nl : nl;
+    long long lo = (MODE == FMODE_R2R ? 2 * sn : sn) * a.seg_len - a.t0 + a.origin;
+    long long hi = lo + (segs - 1) * a.seg_len + G::N;
+    lo = lo > 0 ? lo : 0;
+    hi = hi < a.n_s ? hi : a.n_s;
+    const int esz = MODE == FMODE_R2R ? int(sizeof(R)) : int(sizeof(Cpx<R>));
+    if (hi > lo) {
+      const char* base = MODE == FMODE_R2R ? reinterpret_cast<const char*>(a.xr)
+                                           : reinterpret_cast<const char*>(a.x);
+      uintptr_t b0 = reinterpret_cast<uintptr_t>(base + (lo - a.x_base) * esz);
+      uintptr_t b1 = reinterpret_cast<uintptr_t>(base + (hi - a.x_base) * esz);
+      // stay inside the caller's buffer: whole 16-byte units only
+      b0 = (b0 + 15) & ~uintptr_t(15);
+      b1 &= ~uintptr_t(15);
+      if (b1 > b0) l2_prefetch(reinterpret_cast<const void*>(b0), uint32_t(b1 - b0));
+    }
+  };
+
+  // ---- filter-spectrum staging.  PREF: this thread's VPT vectors of the next filter, in registers
+  float4 hn[C::PREF ? C::VPT : 1];
+  auto fetch = [&](int f) {
+    if constexpr (C::PREF) {
+      const int hb = a.hoff + ((C::ABL & 8) ? (f & 1) : f) * (C::VPT * T);
+      sfor<0, C::VPT>([&](auto uc) {
+        constexpr int u = decltype(uc)::value;
+        hn[u] = tex1Dfetch<float4>(a.htex, hb + spec_vec<R, LOGN>(t, u));
+      });
+    }
+  };
+  // the first item's spectrum and input window are requested before the
+  // table build / TMEM allocation, so their latency overlaps the prologue
+  // (the whole kernel is a few microseconds on small cells)
+  if (blockIdx.x < nitems) {
+    if (tid == 0) prefetch_window(blockIdx.x);
+    int f0 = int(blockIdx.x % nfch) * a.fchunk;
+    if constexpr (TS) {
+      long long g_;
+      int w_;
+      item(blockIdx.x, g_, f0, w_);
+    }
+    fetch(f0);
+  }
+
   if constexpr (C::TMX) {
     if (tid < 32) tmem_alloc<C::TCOLS>(tslot);
     tmem_fence_before();
@@ -821,27 +875,6 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     __syncthreads();  // the exchange buffers are free from here on
   }
 
-  // ---- filter-spectrum staging.  PREF: this thread's VPT vectors of the next filter, in registers
-  float4 hn[C::PREF ? C::VPT : 1];
-  auto fetch = [&](int f) {
-    if constexpr (C::PREF) {
-      const int hb = a.hoff + ((C::ABL & 8) ? (f & 1) : f) * (C::VPT * T);
-      sfor<0, C::VPT>([&](auto uc) {
-        constexpr int u = decltype(uc)::value;
-        hn[u] = tex1Dfetch<float4>(a.htex, hb + spec_vec<R, LOGN>(t, u));
-      });
-    }
-  };
-  if (blockIdx.x < nitems) {
-    int f0 = int(blockIdx.x % nfch) * a.fchunk;
-    if constexpr (TS) {
-      long long g_;
-      int w_;
-      item(blockIdx.x, g_, f0, w_);
-    }
-    fetch(f0);
-  }
-
   const R inv_n = R(1) / R(G::N);
   int xc = 0;
 
@@ -880,38 +913,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     // L2 prefetch of the next item's input window (TMA, one thread): with
     // few filters per segment nothing else hides the DRAM latency of the
     // gather at the start of an item
-    if (tid == 0 && it + gridDim.x < nitems) {
-      long long gn = (it + gridDim.x) / nfch;
-      if constexpr (TS) {
-        int fn_, wn_;
-        item(it + gridDim.x, gn, fn_, wn_);
-      }
-      const long long sn = a.k_lo + gn * C::SEGS;
-      // the next group's live segments only: its window stays inside the
-      // input extent the caller guarantees for [k_lo, k_hi)
-      const long long nl = a.k_hi - sn < C::SEGS ? a.k_hi - sn : C::SEGS;
-      const long long segs = MODE == FMODE_R2R ? 2 * nl : nl;
-      long long lo = (MODE == FMODE_R2R ? 2 * sn : sn) * a.seg_len - a.t0 + a.origin;
-      long long hi = lo + (segs - 1) * a.seg_len + G::N;
-      lo = lo > 0 ? lo : 0;
-      hi = hi < a.n_s ? hi : a.n_s;
-      const int esz = MODE == FMODE_R2R ? int(sizeof(R)) : int(sizeof(Cpx<R>));
-      if (hi > lo) {
-        const char* base = MODE == FMODE_R2R
-                               ? reinterpret_cast<const char*>(a.xr)
-                               : reinterpret_cast<const char*>(a.x);
-        uintptr_t b0 = reinterpret_cast<uintptr_t>(base + (lo - a.x_base) * esz);
-        uintptr_t b1 = reinterpret_cast<uintptr_t>(base + (hi - a.x_base) * esz);
-        b0 &= ~uintptr_t(15);
-        b1 = (b1 + 15) & ~uintptr_t(15);
-        // stay inside the caller's buffer: whole 16-byte units only
-        if (b1 > reinterpret_cast<uintptr_t>(base + (hi - a.x_base) * esz))
-          b1 -= 16;
-        if (b0 < reinterpret_cast<uintptr_t>(base + (lo - a.x_base) * esz))
-          b0 += 16;
-        if (b1 > b0) l2_prefetch(reinterpret_cast<const void*>(b0), uint32_t(b1 - b0));
-      }
-    }
+    if (tid == 0 && it + gridDim.x < nitems) prefetch_window(it + gridDim.x);
     const int f_hi = min(a.n_fil, f_lo + f_w);
     const long long nit = it + gridDim.x;
     int f_next_item = nit < nitems ? int(nit % nfch) * a.fchunk : -1;

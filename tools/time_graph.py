@@ -16,6 +16,13 @@ import paper_1910_01972_b200 as ob  # noqa: E402
 from cases import gen_inputs  # noqa: E402
 from prof_cfg import CFG  # noqa: E402
 
+try:
+    import json
+    with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+        PEAK = float(json.load(f)["hbm_gbs"]) * 1e9
+except Exception:
+    PEAK = 6650e9
+
 for name in sys.argv[1:]:
     ns, m, nfil, n, *_ = CFG[name]
     x, taps = gen_inputs(ns, m, nfil)
@@ -38,4 +45,4 @@ for name in sys.argv[1:]:
     t = float(np.median(ts[1:]))
     byts = 8 * ns * (1 + nfil)
     print(f"variant {os.environ.get('OLSB_VARIANT', '-')} {name}: {t * 1e3:.1f} us "
-          f"{byts / (t * 1e-3) / 6546.6e9 * 100:.1f}% HBM", flush=True)
+          f"{byts / (t * 1e-3) / PEAK * 100:.1f}% HBM", flush=True)
