@@ -227,6 +227,91 @@ using SingleFilterPolicy =
     KCfg<R, LOGN, DefaultPolicy<R, LOGN>::SEGS,
          DefaultPolicy<R, LOGN>::type::NBUF, DefaultPolicy<R, LOGN>::type::HM,
          1, DefaultPolicy<R, LOGN>::type::MINB, 0, 0>;
+
+// warp-per-segment engine for N = 2048 (olsb_w64.cuh), selected with
+// OLSB_W64=1.  Not the default: at 8 warps/SM (252 registers) its FP core
+// alone takes 1.32 ms on cfg3 against the E = 16 engine's 1.05 ms, so
+// halving the exchange traffic and dropping the CTA barriers only reaches
+// parity (1.68 ms)
+inline int w64_env() {
+  static int v = [] {
+    const char* e = getenv("OLSB_W64");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+template <int WPC, int MINB, int MODE>
+int launch_w64_cfg(FusedArgs<float> a, cudaStream_t st) {
+  auto kern = w64::fused_w64_kernel<WPC, MINB, MODE>;
+  constexpr size_t smem = size_t(WPC) * w64::BUF * sizeof(Cpx<float>) + 16;
+  int resident = 0;
+  int rc = prepare(kern, smem, WPC * 32, &resident);
+  if (rc) return rc;
+  // TMEM-allocating kernels: the occupancy API reports 1 CTA/SM
+  resident = std::max(resident, MINB * num_sms());
+  rc = bind_spectra(a, size_t(a.n_fil) * 1024 * 16);
+  if (rc) return rc;
+  const long long nseg = a.k_hi - a.k_lo;
+  const long long warps = (long long)resident * WPC;
+  // whole waves of full-filter items, then the leftover segments in items
+  // of ~n_fil/8 filters so every warp finishes within one small item
+  a.full_items = nseg;
+  a.tchunk = a.n_fil;
+  if (nseg % warps != 0 && a.n_fil >= 2) {
+    a.full_items = (nseg / warps) * warps;
+    const int tdiv = std::min(8, a.n_fil);
+    a.tchunk = (a.n_fil + tdiv - 1) / tdiv;
+  }
+  const long long ntch = (a.n_fil + a.tchunk - 1) / a.tchunk;
+  const long long nitems = a.full_items + (nseg - a.full_items) * ntch;
+  const long long grid = std::min<long long>((nitems + WPC - 1) / WPC, resident);
+  if (grid <= 0) return 0;
+  kern<<<int(grid), WPC * 32, smem, st>>>(a);
+  return int(cudaGetLastError());
+}
+
+// two-warps-per-segment engine for N = 4096 (olsb_w64x2.cuh), selected with
+// OLSB_W64X2=1.  Not the default: parity green and equal to the E = 16
+// engine on the cfg5 shard (21.0 vs 21.1 ms) but slower on cfg2 N = 4096
+// (0.465 vs 0.395 ms, fewer segments than resident slots); like the N = 2048
+// warp-per-segment engine it is held back by 8 warps/SM at 255 registers
+// (profiles/r02_w64x2.log)
+inline int w64x2_env() {
+  static int v = [] {
+    const char* e = getenv("OLSB_W64X2");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+template <int MODE>
+int launch_w64x2(FusedArgs<float> a, cudaStream_t st) {
+  auto kern = w64x2::fused_w64x2_kernel<MODE>;
+  constexpr size_t smem = size_t(2) * w64x2::SBUF * sizeof(Cpx<float>) + 16;
+  int resident = 0;
+  int rc = prepare(kern, smem, 128, &resident);
+  if (rc) return rc;
+  resident = std::max(resident, 2 * num_sms());  // TMEM kernels: see above
+  rc = bind_spectra(a, size_t(a.n_fil) * 2048 * 16);
+  if (rc) return rc;
+  const long long nseg = a.k_hi - a.k_lo;
+  const long long slots = (long long)resident * 2;
+  a.full_items = nseg;
+  a.tchunk = a.n_fil;
+  if (nseg % slots != 0 && a.n_fil >= 2) {
+    a.full_items = (nseg / slots) * slots;
+    const int tdiv = std::min(8, a.n_fil);
+    a.tchunk = (a.n_fil + tdiv - 1) / tdiv;
+  }
+  const long long ntch = (a.n_fil + a.tchunk - 1) / a.tchunk;
+  const long long nitems = a.full_items + (nseg - a.full_items) * ntch;
+  const long long grid = std::min<long long>((nitems + 1) / 2, resident);
+  if (grid <= 0) return 0;
+  kern<<<int(grid), 128, smem, st>>>(a);
+  return int(cudaGetLastError());
+}
+
 template <class R, int LOGN>
 int launch_fused(FusedArgs<R> a, int mode, cudaStream_t st) {
   using D = typename DefaultPolicy<R, LOGN>::type;
