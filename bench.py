@@ -71,10 +71,16 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "20"],
+                 "--format=csv,noheader,nounits", "-lms", "10"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi needs ~0.1-0.3 s to start: wait for its first
+            # sample so the loaded region is actually observed
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 5:
+                time.sleep(0.01)
+            self.lines.clear()
         except Exception:
             self.proc = None
         return self
@@ -364,17 +370,15 @@ def main():
         if ev is not None:
             ev[1].record()
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     kev = [(torch.cuda.Event(enable_timing=True),
             torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    # clocks are sampled from the warm-up through the timed steps (the timed
+    # region alone is ~40 ms, a few nvidia-smi samples)
     with ClockSampler(local) as clk:
+        for _ in range(args.warmup):
+            step()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
