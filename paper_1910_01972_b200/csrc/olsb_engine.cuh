@@ -265,7 +265,7 @@ __device__ __forceinline__ Tw<R> twiddle_value(int q_lo, int i, bool tan01) {
   int idx, l;
   twiddle_decode(q_lo, i, &idx, &l, std::is_same<R, double>::value);
   double c, t;
-  twiddle_entry(q_lo, idx, l, tan01, &c, &t);
+  twiddle_entry_r4(q_lo, idx, l, tan01, &c, &t);
   return Tw<R>{R(c), R(t)};
 }
 

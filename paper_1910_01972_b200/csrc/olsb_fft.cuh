@@ -479,6 +479,75 @@ OLSB_HD void dif_std(Cpx<R>& u, Cpx<R>& v, R c, R s) {
 }
 
 // ---------------------------------------------------------------------------
+// Radix-4 DIT group over stages (j, j + 1) of a runtime window: samples x0..x3
+// at a, a + 2^j, a + 2^(j+1), a + 3 2^j.  With v the stage-(j+1) twiddle of k
+// (and w = v^2 the stage-j twiddle, i v the stage-(j+1) twiddle of k + 2^j):
+//   A, B = x0 +- w x1,   C = v x2,   D = v^3 x3
+//   z0, z2 = A +- (C + D),   z1, z3 = B +- i (C - D)
+// which is the reference's two radix-2 stages exactly (same outputs at the
+// same in-place positions).  In the FMA tangent forms (w x = rho c (x + i t x),
+// rho = 1 GOOD / i ROT) and with C + D = c1 (rho1 P2 + r rho3 P3), r = c3 / c1,
+// a group costs 11 FFMA2 instead of 4 x 3 (Linzer & Feig's radix-4 FMA
+// count).  Table entries: w = (c_w, t_w), v = (c1, t1), v3 = (r, t3); the
+// rho's are compile-time (RW, RV, R3 = ROT).
+// ---------------------------------------------------------------------------
+template <class R>
+OLSB_HD Cpx<R> mul_i(Cpx<R> x) { return Cpx<R>{-x.im, x.re}; }
+
+template <bool RW, bool RV, bool R3, class R>
+OLSB_HD void dit_r4(Cpx<R>& x0, Cpx<R>& x1, Cpx<R>& x2, Cpx<R>& x3, Tw<R> w,
+                    Tw<R> v, Tw<R> v3) {
+#if defined(__CUDA_ARCH__)
+  if constexpr (OLSB_PACKED(R)) {
+    const u64 X0 = pk(x0);
+    Cpx<float> p1 = upk(fma2(pk(x1.im, x1.re), pk(-w.t, w.t), pk(x1)));
+    Cpx<float> p2 = upk(fma2(pk(x2.im, x2.re), pk(-v.t, v.t), pk(x2)));
+    Cpx<float> p3 = upk(fma2(pk(x3.im, x3.re), pk(-v3.t, v3.t), pk(x3)));
+    if constexpr (RW) p1 = mul_i(p1);
+    if constexpr (RV) p2 = mul_i(p2);
+    if constexpr (R3) p3 = mul_i(p3);
+    const u64 A = fma2(pk(p1), pk(w.c, w.c), X0);
+    const u64 B = fma2(pk(p1), pk(-w.c, -w.c), X0);
+    const Cpx<float> sp = upk(fma2(pk(p3), pk(v3.c, v3.c), pk(p2)));
+    const Cpx<float> dm = upk(fma2(pk(p3), pk(-v3.c, -v3.c), pk(p2)));
+    x0 = upk(fma2(pk(sp), pk(v.c, v.c), A));
+    x2 = upk(fma2(pk(sp), pk(-v.c, -v.c), A));
+    x1 = upk(fma2(pk(-dm.im, dm.re), pk(v.c, v.c), B));
+    x3 = upk(fma2(pk(-dm.im, dm.re), pk(-v.c, -v.c), B));
+    return;
+  }
+#endif
+  auto tanf = [](Cpx<R> x, R t) {
+    return Cpx<R>{fmaR(-t, x.im, x.re), fmaR(t, x.re, x.im)};
+  };
+  Cpx<R> p1 = tanf(x1, w.t), p2 = tanf(x2, v.t), p3 = tanf(x3, v3.t);
+  if constexpr (RW) p1 = mul_i(p1);
+  if constexpr (RV) p2 = mul_i(p2);
+  if constexpr (R3) p3 = mul_i(p3);
+  const Cpx<R> A{fmaR(w.c, p1.re, x0.re), fmaR(w.c, p1.im, x0.im)};
+  const Cpx<R> B{fmaR(-w.c, p1.re, x0.re), fmaR(-w.c, p1.im, x0.im)};
+  const Cpx<R> sp{fmaR(v3.c, p3.re, p2.re), fmaR(v3.c, p3.im, p2.im)};
+  const Cpx<R> dm{fmaR(-v3.c, p3.re, p2.re), fmaR(-v3.c, p3.im, p2.im)};
+  const Cpx<R> idm = mul_i(dm);
+  x0 = Cpx<R>{fmaR(v.c, sp.re, A.re), fmaR(v.c, sp.im, A.im)};
+  x2 = Cpx<R>{fmaR(-v.c, sp.re, A.re), fmaR(-v.c, sp.im, A.im)};
+  x1 = Cpx<R>{fmaR(v.c, idm.re, B.re), fmaR(v.c, idm.im, B.im)};
+  x3 = Cpx<R>{fmaR(-v.c, idm.re, B.re), fmaR(-v.c, idm.im, B.im)};
+}
+
+// DIF butterfly with the twiddle i W, W = (c, t) in form ROT_BASE: i W is
+// ROT with the same (c, t) when W is GOOD, GOOD with (-c, t) when W is ROT
+// (used where a table slot holds radix-4 data instead of i W)
+template <bool ROT_BASE, class R>
+OLSB_HD void dif_times_i(Cpx<R>& u, Cpx<R>& v, R c, R t) {
+  if constexpr (ROT_BASE) {
+    dif_good(u, v, -c, t);
+  } else {
+    dif_rot(u, v, c, t);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // window passes.  x[E] are the thread's samples; local index a <-> window bits.
 // ---------------------------------------------------------------------------
 // Junction window (lo = 0, l = 0): all twiddles are compile-time constants.
@@ -547,46 +616,40 @@ struct TwPair {
 
 template <class R, bool TAN01, class TW>
 OLSB_HD void dit_pass_rt(Cpx<R>* x, const TW& tw, int hb) {
-  // j = 0: pairs (2h, 2h + 1), twiddle idx 0
-  {
+  // stages 0, 1: radix-4 groups {a, a+1, a+2, a+3} with w = idx 0, v = idx 1,
+  // v^3 data = idx 2 (forms by hb, warp-uniform under TAN01); without the
+  // tangent forms: radix-2 STD butterflies with idx 0, 1, 2
+  if constexpr (TAN01) {
     const Tw<R> w = tw.get0();
-    if constexpr (TAN01) {
-      if (hb == 1 || hb == 2) {
-        sfor<0, 8>([&](auto hc) {
-          constexpr int a = 2 * decltype(hc)::value;
-          dit_rot(x[a], x[a + 1], w.c, w.t);
-        });
-      } else {
-        sfor<0, 8>([&](auto hc) {
-          constexpr int a = 2 * decltype(hc)::value;
-          dit_good(x[a], x[a + 1], w.c, w.t);
-        });
-      }
+    const TwPair<R> p = tw.get2(1);
+    auto groups = [&](auto rw, auto rv, auto r3) {
+      sfor<0, 4>([&](auto gc) {
+        constexpr int a = 4 * decltype(gc)::value;
+        dit_r4<decltype(rw)::value != 0, decltype(rv)::value != 0,
+               decltype(r3)::value != 0>(x[a], x[a + 1], x[a + 2], x[a + 3],
+                                         w, p.a, p.b);
+      });
+    };
+    // w: ROT iff hb in {1, 2}; v: ROT iff hb >= 2; v^3: ROT iff hb odd
+    if (hb == 0) {
+      groups(IC<0>{}, IC<0>{}, IC<0>{});
+    } else if (hb == 1) {
+      groups(IC<1>{}, IC<0>{}, IC<1>{});
+    } else if (hb == 2) {
+      groups(IC<1>{}, IC<1>{}, IC<0>{});
     } else {
+      groups(IC<0>{}, IC<1>{}, IC<1>{});
+    }
+  } else {
+    {
+      const Tw<R> w = tw.get0();
       sfor<0, 8>([&](auto hc) {
         constexpr int a = 2 * decltype(hc)::value;
         dit_std(x[a], x[a + 1], w.c, w.t);
       });
     }
-  }
-  // j = 1: k = 0 -> idx 1, k = 1 -> idx 2
-  {
-    const TwPair<R> w = tw.get2(1);
-    if constexpr (TAN01) {
-      if (hb >= 2) {
-        sfor<0, 4>([&](auto hc) {
-          constexpr int a = 4 * decltype(hc)::value;
-          dit_rot(x[a], x[a + 2], w.a.c, w.a.t);
-          dit_good(x[a + 1], x[a + 3], w.b.c, w.b.t);
-        });
-      } else {
-        sfor<0, 4>([&](auto hc) {
-          constexpr int a = 4 * decltype(hc)::value;
-          dit_good(x[a], x[a + 2], w.a.c, w.a.t);
-          dit_rot(x[a + 1], x[a + 3], w.b.c, w.b.t);
-        });
-      }
-    } else {
+    {
+      const TwPair<R> w = tw.get2(1);
       sfor<0, 4>([&](auto hc) {
         constexpr int a = 4 * decltype(hc)::value;
         dit_std(x[a], x[a + 2], w.a.c, w.a.t);
@@ -594,44 +657,39 @@ OLSB_HD void dit_pass_rt(Cpx<R>* x, const TW& tw, int hb) {
       });
     }
   }
-  // j = 2, 3: static forms
-  sfor<2, 4>([&](auto jc) {
-    constexpr int j = decltype(jc)::value;
-    sfor<(1 << (j - 1)), (1 << j)>([&](auto pc) {
-      constexpr int pp = decltype(pc)::value;
-      const TwPair<R> w = tw.get2(pp);
-      sfor<0, 2>([&](auto hc2) {
-        constexpr int idx = 2 * pp - 1 + decltype(hc2)::value;
-        constexpr int k = idx - ((1 << j) - 1);
-        const Tw<R> ww = decltype(hc2)::value == 0 ? w.a : w.b;
-        sfor<0, (8 >> j)>([&](auto hc) {
-          constexpr int a = (decltype(hc)::value << (j + 1)) | k;
-          if constexpr (rot_static(j, k)) {
-            dit_rot(x[a], x[a | (1 << j)], ww.c, ww.t);
-          } else {
-            dit_good(x[a], x[a | (1 << j)], ww.c, ww.t);
-          }
-        });
-      });
-    });
+  // stages 2, 3: radix-4 groups {k, k+4, k+8, k+12}, k < 4: w = idx 3 + k,
+  // v = idx 7 + k, v^3 data = idx 11 + k; static forms
+  const TwPair<R> w01 = tw.get2(2), w23 = tw.get2(3);
+  const TwPair<R> v01 = tw.get2(4), v23 = tw.get2(5);
+  const TwPair<R> t01 = tw.get2(6), t23 = tw.get2(7);
+  sfor<0, 4>([&](auto kc) {
+    constexpr int k = decltype(kc)::value;
+    const Tw<R> w = k == 0 ? w01.a : k == 1 ? w01.b : k == 2 ? w23.a : w23.b;
+    const Tw<R> v = k == 0 ? v01.a : k == 1 ? v01.b : k == 2 ? v23.a : v23.b;
+    const Tw<R> t = k == 0 ? t01.a : k == 1 ? t01.b : k == 2 ? t23.a : t23.b;
+    dit_r4<rot_static(2, k), rot_static(3, k), (k & 1) != 0>(
+        x[k], x[k + 4], x[k + 8], x[k + 12], w, v, t);
   });
 }
 
 template <class R, bool TAN01, class TW>
 OLSB_HD void dif_pass_rt(Cpx<R>* x, const TW& tw, int hb) {
-  // j = 3, 2: static forms
+  // j = 3, 2: static forms.  Stage-3 twiddles of k >= 4 are i times those
+  // of k - 4 (their table slots hold the inverse's radix-4 data)
   sfor<0, 2>([&](auto jr) {
     constexpr int j = 3 - decltype(jr)::value;
     sfor<(1 << (j - 1)), (1 << j)>([&](auto pc) {
       constexpr int pp = decltype(pc)::value;
-      const TwPair<R> w = tw.get2(pp);
+      const TwPair<R> w = tw.get2(j == 3 && pp >= 6 ? pp - 2 : pp);
       sfor<0, 2>([&](auto hc2) {
         constexpr int idx = 2 * pp - 1 + decltype(hc2)::value;
         constexpr int k = idx - ((1 << j) - 1);
         const Tw<R> ww = decltype(hc2)::value == 0 ? w.a : w.b;
         sfor<0, (8 >> j)>([&](auto hc) {
           constexpr int a = (decltype(hc)::value << (j + 1)) | k;
-          if constexpr (rot_static(j, k)) {
+          if constexpr (j == 3 && k >= 4) {
+            dif_times_i<rot_static(3, k - 4)>(x[a], x[a | (1 << j)], ww.c, ww.t);
+          } else if constexpr (rot_static(j, k)) {
             dif_rot(x[a], x[a | (1 << j)], ww.c, ww.t);
           } else {
             dif_good(x[a], x[a | (1 << j)], ww.c, ww.t);
@@ -640,7 +698,7 @@ OLSB_HD void dif_pass_rt(Cpx<R>* x, const TW& tw, int hb) {
       });
     });
   });
-  // j = 1
+  // j = 1 (k = 1: i times the k = 0 twiddle; its slot holds radix-4 data)
   {
     const TwPair<R> w = tw.get2(1);
     if constexpr (TAN01) {
@@ -648,13 +706,13 @@ OLSB_HD void dif_pass_rt(Cpx<R>* x, const TW& tw, int hb) {
         sfor<0, 4>([&](auto hc) {
           constexpr int a = 4 * decltype(hc)::value;
           dif_rot(x[a], x[a + 2], w.a.c, w.a.t);
-          dif_good(x[a + 1], x[a + 3], w.b.c, w.b.t);
+          dif_times_i<true>(x[a + 1], x[a + 3], w.a.c, w.a.t);
         });
       } else {
         sfor<0, 4>([&](auto hc) {
           constexpr int a = 4 * decltype(hc)::value;
           dif_good(x[a], x[a + 2], w.a.c, w.a.t);
-          dif_rot(x[a + 1], x[a + 3], w.b.c, w.b.t);
+          dif_times_i<false>(x[a + 1], x[a + 3], w.a.c, w.a.t);
         });
       }
     } else {
@@ -836,6 +894,43 @@ OLSB_HD void twiddle_entry(int lo, int idx, int l, bool tan01, double* c,
     *c = co;
     *t = s / co;
   }
+}
+
+// Runtime-window table entry idx for the radix-4 inverse (dit_pass_rt): as
+// twiddle_entry, except the slots of the stage-(j+1) twiddles i v of
+// k + 2^j, which the radix-4 groups do not need, hold the groups' v^3 data
+// (r = c3 / c1, t3): idx 11 + k for the stage-(2, 3) group k, and idx 2 for
+// the stage-(0, 1) group when the tangent forms are on.  v^3's form is static
+// (ROT iff k, or hb, is odd), |t3| <= tan(3 pi / 8).
+OLSB_HD void twiddle_entry_r4(int lo, int idx, int l, bool tan01, double* c,
+                              double* t) {
+  const bool g23 = idx >= 11 && idx <= 14;
+  const bool g01 = idx == 2 && tan01;
+  if (!g23 && !g01) {
+    twiddle_entry(lo, idx, l, tan01, c, t);
+    return;
+  }
+  const int k = g23 ? idx - 11 : 0;
+  const int j1 = g23 ? 3 : 1;                      // stage of v
+  const int hb = lo >= 2 ? (l >> (lo - 2)) & 3 : 0;
+  const double num = double(k) * double(1 << lo) + double(l);
+  const double den = double(1 << (lo + j1));
+  double s1, c1, s3, c3;
+#if defined(__CUDA_ARCH__)
+  sincospi(num / den, &s1, &c1);
+  sincospi(3.0 * num / den, &s3, &c3);
+#else
+  const double th = 3.14159265358979323846 * (num / den);
+  s1 = std::sin(th);
+  c1 = std::cos(th);
+  s3 = std::sin(3.0 * th);
+  c3 = std::cos(3.0 * th);
+#endif
+  const bool rot_v = g23 ? rot_static(3, k) : hb >= 2;
+  const bool rot_3 = ((g23 ? k : hb) & 1) != 0;
+  const double cv = rot_v ? s1 : c1;
+  *c = (rot_3 ? s3 : c3) / cv;
+  *t = rot_3 ? -c3 / s3 : s3 / c3;
 }
 
 // entry i of window lo's table -> (idx or -1, l)

@@ -36,7 +36,7 @@ static void run(const R* in, R* out, bool inverse) {
         const int l = G::low_bits(q, t);
         for (int i = 0; i < 15; ++i) {
           double c, tt;
-          twiddle_entry(G::lo(q), i, l, G::tan01(q), &c, &tt);
+          twiddle_entry_r4(G::lo(q), i, l, G::tan01(q), &c, &tt);
           acc.tw[i] = Tw<R>{R(c), R(tt)};
         }
         const int hb = G::lo(q) >= 2 ? (l >> (G::lo(q) - 2)) & 3 : 0;
