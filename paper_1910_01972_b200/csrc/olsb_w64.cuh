@@ -31,6 +31,13 @@
 
 #include "olsb_engine.cuh"
 
+// compile-time ablation bits for bottleneck analysis (results wrong when
+// set): 2 no exchange shared-memory traffic, 4 no output staging; build with
+// OLSB_NVCC_EXTRA=-DOLSB_W64_ABL=k (output writes: OLSB_DEBUG=1 at run time)
+#ifndef OLSB_W64_ABL
+#define OLSB_W64_ABL 0
+#endif
+
 namespace olsb {
 namespace w64 {
 
@@ -463,7 +470,7 @@ __global__ void __launch_bounds__(WPC * 32, MINB)
       // ---- the exchange (warp-local)
       if (lane == 0) bulk_wait_read();  // the previous filter's bulk store
       __syncwarp();
-      if (!(a.dbg & 2)) store_a(buf, lane, y);  // dbg 2: ablation, no exchange
+      if (!(OLSB_W64_ABL & 2)) store_a(buf, lane, y);  // ablation: no exchange
       __syncwarp();
       // ---- window B, batch by batch; outputs staged at natural position
       // p + delta, delta chosen so staged and global element addresses agree
@@ -474,7 +481,7 @@ __global__ void __launch_bounds__(WPC * 32, MINB)
       const int delta = ((galign - a.t0) % EPV + EPV) % EPV;
       auto stage_out = [&](auto bc, const Cpx<float>* z) {
         constexpr int b = decltype(bc)::value;
-        if (a.dbg & 4) return;  // ablation: no staging
+        if (OLSB_W64_ABL & 4) return;  // ablation: no staging
         if constexpr (MODE == FMODE_C2C) {
           Cpx<float>* stg = buf + delta + 32 * b + lane;
           sfor<0, 32>([&](auto hc) {
@@ -491,7 +498,7 @@ __global__ void __launch_bounds__(WPC * 32, MINB)
       };
       Cpx<float>* y0 = y;
       Cpx<float>* y1 = y + 32;
-      if (!(a.dbg & 2)) load_b(buf, lane, y);
+      if (!(OLSB_W64_ABL & 2)) load_b(buf, lane, y);
       inv_window_b<0>(y0, tt, [&] { if (more) fetch(h0, f + 1, 0); });
       __syncwarp();  // every lane's exchange reads precede the staging
       stage_out(IC<0>{}, y0);
