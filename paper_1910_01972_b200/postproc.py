@@ -1,9 +1,12 @@
 """Post-processing specs (reference: olsconv/postproc.py:12-38).
 
-``none`` and ``scale`` are fused into the engine's writeback (C-ABI pp_kind
-0/1).  ``magnitude_squared`` and ``derivative`` (the reference's non-local
-epilogues, postproc.py:44-85 / _kernels_nb.py:224-262) are SURVEY §8(f)3
-"next" rows; the engine rejects them with EngineError until they land.
+All four kinds are fused into the engine's writeback (C-ABI pp_kind 0-3):
+``none`` and ``scale`` (_store kinds 0/1, _kernels_nb.py:218-226),
+``magnitude_squared`` (|y|^2 real rows, olsb_fused_c2c_abs2 / fused_r2r
+pp_kind 2, _kernels_nb.py:288-337) and ``derivative`` (the non-local
+epilogue with the halo geometry, _kernels_nb.py:224-262; tap length 1 falls
+back to the plain engine plus a device-side global difference, ols.py).
+The host streaming and range paths take every kind but ``derivative``.
 """
 
 from __future__ import annotations
