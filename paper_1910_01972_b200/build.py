@@ -26,7 +26,7 @@ LIB = os.path.join(PKG, "libolsb.so")
 SOURCES = [os.path.join(CSRC, "olsb_kernels.cu"),
            os.path.join(CSRC, "olsb_inst.cu")]
 HEADERS = [os.path.join(CSRC, h) for h in
-           ("olsb_fft.cuh", "olsb_engine.cuh", "olsb_w64.cuh", "olsb_w64x2.cuh", "olsb_launch.cuh")] + [
+           ("olsb_fft.cuh", "olsb_engine.cuh", "olsb_w64.cuh", "olsb_w64x2.cuh", "olsb_w32x2.cuh", "olsb_launch.cuh")] + [
     os.path.join(INCLUDE, "olsb.h")]
 LOGNS = range(2, 13)
 OBJDIR = os.path.join(PKG, "build_obj")

@@ -16,6 +16,7 @@
 #include "olsb_engine.cuh"
 #include "olsb_w64.cuh"
 #include "olsb_w64x2.cuh"
+#include "olsb_w32x2.cuh"
 
 namespace olsb {
 
@@ -312,6 +313,44 @@ int launch_w64x2(FusedArgs<float> a, cudaStream_t st) {
   return int(cudaGetLastError());
 }
 
+// two-warps-per-segment E = 32 engine for N = 2048 (olsb_w32x2.cuh),
+// OLSB_W32X2=1
+inline int w32x2_env() {
+  static int v = [] {
+    const char* e = getenv("OLSB_W32X2");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+template <int MODE>
+int launch_w32x2(FusedArgs<float> a, cudaStream_t st) {
+  auto kern = w32x2::fused_w32x2_kernel<MODE>;
+  constexpr size_t smem = size_t(w32x2::SEGS) * w32x2::SBUF * sizeof(Cpx<float>) + 16;
+  int resident = 0;
+  int rc = prepare(kern, smem, w32x2::WARPS * 32, &resident);
+  if (rc) return rc;
+  resident = std::max(resident, num_sms());  // TMEM kernels: see above
+  rc = bind_spectra(a, size_t(a.n_fil) * 1024 * 16);
+  if (rc) return rc;
+  const long long nseg = a.k_hi - a.k_lo;
+  const long long slots = (long long)resident * w32x2::SEGS;
+  a.full_items = nseg;
+  a.tchunk = a.n_fil;
+  if (nseg % slots != 0 && a.n_fil >= 2) {
+    a.full_items = (nseg / slots) * slots;
+    const int tdiv = std::min(8, a.n_fil);
+    a.tchunk = (a.n_fil + tdiv - 1) / tdiv;
+  }
+  const long long ntch = (a.n_fil + a.tchunk - 1) / a.tchunk;
+  const long long nitems = a.full_items + (nseg - a.full_items) * ntch;
+  const long long grid =
+      std::min<long long>((nitems + w32x2::SEGS - 1) / w32x2::SEGS, resident);
+  if (grid <= 0) return 0;
+  kern<<<int(grid), w32x2::WARPS * 32, smem, st>>>(a);
+  return int(cudaGetLastError());
+}
+
 template <class R, int LOGN>
 int launch_fused(FusedArgs<R> a, int mode, cudaStream_t st) {
   using D = typename DefaultPolicy<R, LOGN>::type;
@@ -323,6 +362,11 @@ int launch_fused(FusedArgs<R> a, int mode, cudaStream_t st) {
     }
   }
   if constexpr (std::is_same<R, float>::value && LOGN == 11) {
+    if (!a.xtw && variant_env() < 0 && w32x2_env() &&
+        (a.pp_kind == OLSB_PP_NONE || a.pp_kind == OLSB_PP_SCALE)) {
+      if (mode == FMODE_C2C) return launch_w32x2<FMODE_C2C>(a, st);
+      if (mode == FMODE_ABS2) return launch_w32x2<FMODE_ABS2>(a, st);
+    }
     if (!a.xtw && variant_env() < 0 && w64_env() &&
         (a.pp_kind == OLSB_PP_NONE || a.pp_kind == OLSB_PP_SCALE)) {
       if (mode == FMODE_C2C) return launch_w64_cfg<4, 2, FMODE_C2C>(a, st);
