@@ -493,46 +493,55 @@ OLSB_HD void dif_std(Cpx<R>& u, Cpx<R>& v, R c, R s) {
 // ---------------------------------------------------------------------------
 template <class R>
 OLSB_HD Cpx<R> mul_i(Cpx<R> x) { return Cpx<R>{-x.im, x.re}; }
+// x * i^Q (Q mod 4): a half swap and / or negations, which ptxas folds into
+// the operand modifiers of an FFMA2 multiplicand
+template <int Q, class R>
+OLSB_HD Cpx<R> rot_q(Cpx<R> x) {
+  constexpr int q = ((Q % 4) + 4) % 4;
+  if constexpr (q == 0) return x;
+  if constexpr (q == 1) return Cpx<R>{-x.im, x.re};
+  if constexpr (q == 2) return Cpx<R>{-x.re, -x.im};
+  return Cpx<R>{x.im, -x.re};
+}
 
+// (the rotations rho are kept on FFMA2 multiplicands only -- an addend cannot
+// carry swap / negate modifiers:  C + D = c1 rho1 (P2 + r (rho3 / rho1) P3))
 template <bool RW, bool RV, bool R3, class R>
 OLSB_HD void dit_r4(Cpx<R>& x0, Cpx<R>& x1, Cpx<R>& x2, Cpx<R>& x3, Tw<R> w,
                     Tw<R> v, Tw<R> v3) {
+  constexpr int QW = RW ? 1 : 0, Q1 = RV ? 1 : 0, Q3 = (R3 ? 1 : 0) - Q1;
 #if defined(__CUDA_ARCH__)
   if constexpr (OLSB_PACKED(R)) {
     const u64 X0 = pk(x0);
-    Cpx<float> p1 = upk(fma2(pk(x1.im, x1.re), pk(-w.t, w.t), pk(x1)));
-    Cpx<float> p2 = upk(fma2(pk(x2.im, x2.re), pk(-v.t, v.t), pk(x2)));
-    Cpx<float> p3 = upk(fma2(pk(x3.im, x3.re), pk(-v3.t, v3.t), pk(x3)));
-    if constexpr (RW) p1 = mul_i(p1);
-    if constexpr (RV) p2 = mul_i(p2);
-    if constexpr (R3) p3 = mul_i(p3);
-    const u64 A = fma2(pk(p1), pk(w.c, w.c), X0);
-    const u64 B = fma2(pk(p1), pk(-w.c, -w.c), X0);
-    const Cpx<float> sp = upk(fma2(pk(p3), pk(v3.c, v3.c), pk(p2)));
-    const Cpx<float> dm = upk(fma2(pk(p3), pk(-v3.c, -v3.c), pk(p2)));
-    x0 = upk(fma2(pk(sp), pk(v.c, v.c), A));
-    x2 = upk(fma2(pk(sp), pk(-v.c, -v.c), A));
-    x1 = upk(fma2(pk(-dm.im, dm.re), pk(v.c, v.c), B));
-    x3 = upk(fma2(pk(-dm.im, dm.re), pk(-v.c, -v.c), B));
+    const Cpx<float> p1 = upk(fma2(pk(x1.im, x1.re), pk(-w.t, w.t), pk(x1)));
+    const Cpx<float> p2 = upk(fma2(pk(x2.im, x2.re), pk(-v.t, v.t), pk(x2)));
+    const Cpx<float> p3 = upk(fma2(pk(x3.im, x3.re), pk(-v3.t, v3.t), pk(x3)));
+    const u64 A = fma2(pk(rot_q<QW>(p1)), pk(w.c, w.c), X0);
+    const u64 B = fma2(pk(rot_q<QW>(p1)), pk(-w.c, -w.c), X0);
+    const Cpx<float> sp = upk(fma2(pk(rot_q<Q3>(p3)), pk(v3.c, v3.c), pk(p2)));
+    const Cpx<float> dm = upk(fma2(pk(rot_q<Q3>(p3)), pk(-v3.c, -v3.c), pk(p2)));
+    x0 = upk(fma2(pk(rot_q<Q1>(sp)), pk(v.c, v.c), A));
+    x2 = upk(fma2(pk(rot_q<Q1>(sp)), pk(-v.c, -v.c), A));
+    x1 = upk(fma2(pk(rot_q<Q1 + 1>(dm)), pk(v.c, v.c), B));
+    x3 = upk(fma2(pk(rot_q<Q1 + 1>(dm)), pk(-v.c, -v.c), B));
     return;
   }
 #endif
   auto tanf = [](Cpx<R> x, R t) {
     return Cpx<R>{fmaR(-t, x.im, x.re), fmaR(t, x.re, x.im)};
   };
-  Cpx<R> p1 = tanf(x1, w.t), p2 = tanf(x2, v.t), p3 = tanf(x3, v3.t);
-  if constexpr (RW) p1 = mul_i(p1);
-  if constexpr (RV) p2 = mul_i(p2);
-  if constexpr (R3) p3 = mul_i(p3);
-  const Cpx<R> A{fmaR(w.c, p1.re, x0.re), fmaR(w.c, p1.im, x0.im)};
-  const Cpx<R> B{fmaR(-w.c, p1.re, x0.re), fmaR(-w.c, p1.im, x0.im)};
-  const Cpx<R> sp{fmaR(v3.c, p3.re, p2.re), fmaR(v3.c, p3.im, p2.im)};
-  const Cpx<R> dm{fmaR(-v3.c, p3.re, p2.re), fmaR(-v3.c, p3.im, p2.im)};
-  const Cpx<R> idm = mul_i(dm);
-  x0 = Cpx<R>{fmaR(v.c, sp.re, A.re), fmaR(v.c, sp.im, A.im)};
-  x2 = Cpx<R>{fmaR(-v.c, sp.re, A.re), fmaR(-v.c, sp.im, A.im)};
-  x1 = Cpx<R>{fmaR(v.c, idm.re, B.re), fmaR(v.c, idm.im, B.im)};
-  x3 = Cpx<R>{fmaR(-v.c, idm.re, B.re), fmaR(-v.c, idm.im, B.im)};
+  auto axpy = [](R c, Cpx<R> x, Cpx<R> y) {
+    return Cpx<R>{fmaR(c, x.re, y.re), fmaR(c, x.im, y.im)};
+  };
+  const Cpx<R> p1 = rot_q<QW>(tanf(x1, w.t));
+  const Cpx<R> p2 = tanf(x2, v.t);
+  const Cpx<R> p3 = rot_q<Q3>(tanf(x3, v3.t));
+  const Cpx<R> A = axpy(w.c, p1, x0), B = axpy(-w.c, p1, x0);
+  const Cpx<R> sp = axpy(v3.c, p3, p2), dm = axpy(-v3.c, p3, p2);
+  x0 = axpy(v.c, rot_q<Q1>(sp), A);
+  x2 = axpy(-v.c, rot_q<Q1>(sp), A);
+  x1 = axpy(v.c, rot_q<Q1 + 1>(dm), B);
+  x3 = axpy(-v.c, rot_q<Q1 + 1>(dm), B);
 }
 
 // DIF butterfly with the twiddle i W, W = (c, t) in form ROT_BASE: i W is
