@@ -110,7 +110,7 @@ int olsb_fused_c2c(const void* x, int64_t x_base, int64_t n_s,
  * `out_base` as in olsb_fused_c2c; the input samples a call reads are
  * [x_lo, x_hi) of olsb_input_extent (clipped to [0, n_s)).  pp_kind
  * OLSB_PP_MAG2 selects the |y|^2 epilogue of olsb_fused_c2c_abs2: `out` is
- * then REAL. */
+ * then REAL.  OLSB_PP_DERIV uses the halo geometry (olsb_input_extent_pp). */
 int olsb_fused_c2c_range(const void* x, int64_t x_base, int64_t n_s,
                          const void* spectra_dev, int n_fil, int n, int m,
                          int origin, int64_t g_lo, int64_t g_hi, int pp_kind,
@@ -194,6 +194,14 @@ int olsb_filter_spectra_c2c_ref(const void* taps, int n_fil, int m, int n,
  * (before clipping to [0, n_s)): the shard plus its halos. */
 int olsb_input_extent(int n, int m, int origin, int64_t g_lo, int64_t g_hi,
                       int64_t* x_lo, int64_t* x_hi);
+
+/* Input extent of a range call with post-processing pp_kind (mode 0: the
+ * c2c range entry, 1: the r2r one).  OLSB_PP_DERIV ranges use the halo
+ * geometry (t0 = m, L = n - m - 1: each output's neighbours lie in its own
+ * segment), which reads one more sample on each side. */
+int olsb_input_extent_pp(int mode, int n, int m, int origin, int pp_kind,
+                         int64_t g_lo, int64_t g_hi, int64_t* x_lo,
+                         int64_t* x_hi);
 
 /* Input samples [*x_lo, *x_hi) that olsb_fused_r2r_range(g_lo, g_hi) reads:
  * the windows of whole segment pairs (both halves of a pair are always

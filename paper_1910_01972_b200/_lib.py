@@ -58,6 +58,9 @@ SIGNATURES = {
                                      c_vp, c_i64, c_i64, c_int, c_vp]),
     "olsb_input_extent": (c_int, [c_int, c_int, c_int, c_i64, c_i64,
                                   ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
+    "olsb_input_extent_pp": (c_int, [c_int, c_int, c_int, c_int, c_int, c_i64,
+                                     c_i64, ctypes.POINTER(c_i64),
+                                     ctypes.POINTER(c_i64)]),
     "olsb_input_extent_r2r": (c_int, [c_int, c_int, c_int, c_i64, c_i64,
                                       ctypes.POINTER(c_i64),
                                       ctypes.POINTER(c_i64)]),

@@ -433,19 +433,38 @@ int olsb_fused_r2r(const void* x, int64_t x_base, int64_t n_s,
                      out, out_ld, out_base, precision, stream);
 }
 
+// Segment geometry of the range entries: the plain one (t0 = m - 1, L = n -
+// m + 1), or for the derivative the halo geometry (t0 = m, L = n - m - 1):
+// every output's neighbours are then in-place samples of its own segment
+// (ols.py:137-146 with halo 1; for m = 1 too, where the reference instead
+// recomputes seam neighbours from the input)
+static int range_geometry(int pp_kind, int n, int m, int* t0, int64_t* l_eff) {
+  *t0 = m - 1;
+  *l_eff = n - m + 1;
+  if (pp_kind == OLSB_PP_DERIV) {
+    *t0 = m;
+    *l_eff = n - m - 1;
+    if (*l_eff < 1) return OLSB_E_GEOMETRY;
+  }
+  return 0;
+}
+
 int olsb_fused_c2c_range(const void* x, int64_t x_base, int64_t n_s,
                          const void* spectra_dev, int n_fil, int n, int m,
                          int origin, int64_t g_lo, int64_t g_hi, int pp_kind,
                          double pp_c, void* out, int64_t out_ld,
                          int64_t out_base, int precision, void* stream) {
   if (m < 1 || m > n || origin < 0 || origin >= m) return OLSB_E_BAD_ARG;
+  int t0;
+  int64_t le;
+  if (int rc = range_geometry(pp_kind, n, m, &t0, &le)) return rc;
   // magnitude_squared: the |y|^2 epilogue into a REAL out
   if (pp_kind == OLSB_PP_MAG2)
     return fused_range(FMODE_ABS2, x, x_base, n_s, spectra_dev, n_fil, n,
                        m - 1, origin, n - m + 1, g_lo, g_hi, OLSB_PP_NONE, 1.0,
                        out, out_ld, out_base, precision, stream);
-  return fused_range(FMODE_C2C, x, x_base, n_s, spectra_dev, n_fil, n, m - 1,
-                     origin, n - m + 1, g_lo, g_hi, pp_kind, pp_c, out, out_ld,
+  return fused_range(FMODE_C2C, x, x_base, n_s, spectra_dev, n_fil, n, t0,
+                     origin, le, g_lo, g_hi, pp_kind, pp_c, out, out_ld,
                      out_base, precision, stream);
 }
 
@@ -455,20 +474,27 @@ int olsb_fused_r2r_range(const void* x, int64_t x_base, int64_t n_s,
                          double pp_c, void* out, int64_t out_ld,
                          int64_t out_base, int precision, void* stream) {
   if (m < 1 || m > n || origin < 0 || origin >= m) return OLSB_E_BAD_ARG;
-  return fused_range(FMODE_R2R, x, x_base, n_s, spectra_dev, n_fil, n, m - 1,
-                     origin, n - m + 1, g_lo, g_hi, pp_kind, pp_c, out, out_ld,
+  int t0;
+  int64_t le;
+  if (int rc = range_geometry(pp_kind, n, m, &t0, &le)) return rc;
+  return fused_range(FMODE_R2R, x, x_base, n_s, spectra_dev, n_fil, n, t0,
+                     origin, le, g_lo, g_hi, pp_kind, pp_c, out, out_ld,
                      out_base, precision, stream);
 }
 
 static int input_extent(int mode, int n, int m, int origin, int64_t g_lo,
-                        int64_t g_hi, int64_t* x_lo, int64_t* x_hi) {
+                        int64_t g_hi, int64_t* x_lo, int64_t* x_hi,
+                        int pp_kind = OLSB_PP_NONE) {
   if (log2_of(n) < 0) return OLSB_E_BAD_LENGTH;
   if (m < 1 || m > n || origin < 0 || origin >= m || g_hi < g_lo || !x_lo ||
       !x_hi)
     return OLSB_E_BAD_ARG;
+  int t0;
+  int64_t l_eff;
+  if (int rc = range_geometry(pp_kind, n, m, &t0, &l_eff)) return rc;
   int t0e;
   long long le;
-  engine_grid(n, m - 1, n - m + 1, &t0e, &le);
+  engine_grid(n, t0, l_eff, &t0e, &le);
   long long k_lo = g_lo / le, k_hi = (g_hi + le - 1) / le;
   if (mode == FMODE_R2R) {  // whole segment pairs {2k, 2k + 1}
     k_lo = (k_lo / 2) * 2;
@@ -487,6 +513,13 @@ int olsb_input_extent(int n, int m, int origin, int64_t g_lo, int64_t g_hi,
 int olsb_input_extent_r2r(int n, int m, int origin, int64_t g_lo,
                           int64_t g_hi, int64_t* x_lo, int64_t* x_hi) {
   return input_extent(FMODE_R2R, n, m, origin, g_lo, g_hi, x_lo, x_hi);
+}
+
+int olsb_input_extent_pp(int mode, int n, int m, int origin, int pp_kind,
+                         int64_t g_lo, int64_t g_hi, int64_t* x_lo,
+                         int64_t* x_hi) {
+  if (mode != FMODE_C2C && mode != FMODE_R2R) return OLSB_E_BAD_ARG;
+  return input_extent(mode, n, m, origin, g_lo, g_hi, x_lo, x_hi, pp_kind);
 }
 
 int olsb_copy2d_async(void* dst, int64_t dst_pitch_bytes, const void* src,

@@ -43,9 +43,6 @@ class Executor:
         if filters.origin != seg_plan.origin:
             raise PlanMismatch(
                 f"filter origin {filters.origin} != plan {seg_plan.origin}")
-        if pp.kind == "derivative" and seg_plan.tap_len == 1:
-            raise EngineError("derivative with one tap has no fused epilogue; "
-                              "use convolve()")
         if seg_plan.mode == "r2r" and filters.value_kind != "real":
             raise PlanMismatch("complex filter taps on the real path")
         layout = _required_layout(seg_plan.mode, "fused")
@@ -62,11 +59,21 @@ class Executor:
         self.device = self.spec_dev.device
         self.n_fil = filters.n_filters
         l_eff, t0, win_off, n_seg = _geometry(seg_plan, pp.halo)
-        self._entry = getattr(_lib.load(), _engine_entry(seg_plan, pp))
-        self._abs2 = _engine_entry(seg_plan, pp) == "olsb_fused_c2c_abs2"
-        self._head = (seg_plan.signal_len, self.spec_dev.data_ptr(),
-                      self.n_fil, seg_plan.fft_len, seg_plan.tap_len,
-                      seg_plan.origin, l_eff, t0, win_off, 0, n_seg)
+        if pp.kind == "derivative" and seg_plan.tap_len == 1:
+            # one tap: the range entry's halo geometry (as convolve())
+            name = ("olsb_fused_r2r_range" if seg_plan.mode == "r2r"
+                    else "olsb_fused_c2c_range")
+            self._entry = getattr(_lib.load(), name)
+            self._abs2 = False
+            self._head = (seg_plan.signal_len, self.spec_dev.data_ptr(),
+                          self.n_fil, seg_plan.fft_len, seg_plan.tap_len,
+                          seg_plan.origin, 0, seg_plan.signal_len)
+        else:
+            self._entry = getattr(_lib.load(), _engine_entry(seg_plan, pp))
+            self._abs2 = _engine_entry(seg_plan, pp) == "olsb_fused_c2c_abs2"
+            self._head = (seg_plan.signal_len, self.spec_dev.data_ptr(),
+                          self.n_fil, seg_plan.fft_len, seg_plan.tap_len,
+                          seg_plan.origin, l_eff, t0, win_off, 0, n_seg)
         self._pp = () if self._abs2 else (pp.code, float(pp.scale))
         real_in = seg_plan.mode == "r2r"
         real_out = real_in or pp.real_output

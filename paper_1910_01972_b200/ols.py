@@ -330,11 +330,9 @@ def convolve(signal: Signal, filters: FilterSet, seg_plan: SegmentPlan,
         raise EngineError("variant 'fused_exact' (the reference's arithmetic) "
                           "covers c2c with postproc none | scale | "
                           "magnitude_squared")
-    if pp.kind == "derivative" and (seg_plan.tap_len == 1
-                                    or variant != "fused"):
-        # M = 1 has no halo (the reference recomputes seam neighbours from the
-        # input, _kernels_nb.py:232-260); the comparison variants have no
-        # segment epilogue: plain result, then the global difference on device
+    if pp.kind == "derivative" and variant != "fused":
+        # the comparison variants have no segment epilogue: plain result,
+        # then the global difference on the device
         plain = convolve(signal, filters, seg_plan, variant, None, workers)
         return _derivative(plain, out)
 
@@ -385,9 +383,6 @@ def convolve(signal: Signal, filters: FilterSet, seg_plan: SegmentPlan,
     if variant == "fused":
         spec_dev = _engine_spectra(filters)
         if out is not None and not out.is_cuda:
-            if pp.kind == "derivative":
-                raise EngineError("the host streaming path has no 'derivative' "
-                                  "epilogue; convolve into device memory")
             return _fused_streaming(signal, spec_dev, seg_plan, pp, precision,
                                     l_eff, t0, win_off, n_seg_eff, out,
                                     chunk_segments)
@@ -398,6 +393,17 @@ def convolve(signal: Signal, filters: FilterSet, seg_plan: SegmentPlan,
             out = torch.empty((n_fil, n_s), dtype=out_dtype,
                               device=signal.samples.device)
         with torch.cuda.device(signal.samples.device):
+            if pp.kind == "derivative" and seg_plan.tap_len == 1:
+                # one tap has no aliased region to hold a halo in the
+                # reference's geometry (it recomputes seam neighbours from
+                # the input, _kernels_nb.py:232-260); the range entries'
+                # halo geometry (t0 = 1, L = N - 2) keeps both neighbours in
+                # the segment
+                for lo, hi in _chunk_bounds(n_s, workers):
+                    fused_range_launch(signal.samples, 0, n_s, spec_dev, n_fil,
+                                       seg_plan, lo, hi, pp, out, n_s, 0,
+                                       precision)
+                return out
             for lo, hi in _chunk_bounds(n_seg_eff, workers):
                 fused_launch(signal.samples, 0, n_s, spec_dev, n_fil, seg_plan,
                              l_eff, t0, win_off, lo, hi, pp, out, n_s, 0,
@@ -517,28 +523,32 @@ def fused_range_launch(x: torch.Tensor, x_base: int, n_s: int,
                        out_base: int, precision: Precision,
                        stream: Optional[int] = None) -> None:
     """Outputs [g_lo, g_hi) through olsb_fused_{c2c,r2r}_range (shards,
-    streams)."""
+    streams).  Every post-process; the derivative runs in the halo geometry
+    (t0 = M, L = N - M - 1), whose input extent input_extent(..., pp)
+    gives."""
     entry = ("olsb_fused_r2r_range" if seg_plan.mode == "r2r"
              else "olsb_fused_c2c_range")
-    if pp.kind not in ("none", "scale", "magnitude_squared"):
-        raise EngineError(f"range launches support postproc none|scale|"
-                          f"magnitude_squared, got {pp.kind!r}")
+    if pp.kind == "derivative" and seg_plan.fft_len - seg_plan.tap_len - 1 < 1:
+        raise HaloUnavailable(
+            f"segment length {seg_plan.fft_len} leaves no room for a halo of 1"
+            f" around {seg_plan.tap_len} taps")
     _lib.call(entry, x.data_ptr(), x_base, n_s, spec_dev.data_ptr(), n_fil,
               seg_plan.fft_len, seg_plan.tap_len, seg_plan.origin, g_lo, g_hi,
               pp.code, float(pp.scale), out.data_ptr(), out_ld, out_base,
               precision.code, _stream_ptr() if stream is None else stream)
 
 
-def input_extent(seg_plan: SegmentPlan, g_lo: int, g_hi: int) -> Tuple[int, int]:
-    """Input samples [x_lo, x_hi) the engine reads to produce outputs
-    [g_lo, g_hi) (its shard plus halos; clip to [0, n_s) before copying)."""
+def input_extent(seg_plan: SegmentPlan, g_lo: int, g_hi: int,
+                 postproc: PostProcSpec = NONE) -> Tuple[int, int]:
+    """Input samples [x_lo, x_hi) the engine's range entry reads to produce
+    outputs [g_lo, g_hi) with post-process `postproc` (its shard plus halos;
+    clip to [0, n_s) before copying)."""
     import ctypes
     lo, hi = ctypes.c_int64(), ctypes.c_int64()
-    fn = ("olsb_input_extent_r2r" if seg_plan.mode == "r2r"
-          else "olsb_input_extent")
-    _lib.check(getattr(_lib.load(), fn)(
-        seg_plan.fft_len, seg_plan.tap_len, seg_plan.origin, g_lo, g_hi,
-        ctypes.byref(lo), ctypes.byref(hi)), fn)
+    _lib.check(_lib.load().olsb_input_extent_pp(
+        1 if seg_plan.mode == "r2r" else 0, seg_plan.fft_len,
+        seg_plan.tap_len, seg_plan.origin, postproc.code, g_lo, g_hi,
+        ctypes.byref(lo), ctypes.byref(hi)), "olsb_input_extent_pp")
     return lo.value, hi.value
 
 
@@ -573,7 +583,7 @@ def _fused_streaming(signal, spec_dev, seg_plan, pp, precision, l_eff, t0,
     w = max(32, (chunk_segments * l_eff) // 32 * 32)
     chunks = [(g, min(g + w, n_s)) for g in range(0, n_s, w)]
     nslot = min(3, len(chunks))
-    ext = [input_extent(seg_plan, ga, gb) for ga, gb in chunks]
+    ext = [input_extent(seg_plan, ga, gb, pp) for ga, gb in chunks]
     x_len_max = max(min(hi, n_s) - max(lo, 0) for lo, hi in ext)
     with torch.cuda.device(dev):
         streams = [torch.cuda.Stream() for _ in range(nslot)]

@@ -4,9 +4,10 @@ All four kinds are fused into the engine's writeback (C-ABI pp_kind 0-3):
 ``none`` and ``scale`` (_store kinds 0/1, _kernels_nb.py:218-226),
 ``magnitude_squared`` (|y|^2 real rows, olsb_fused_c2c_abs2 / fused_r2r
 pp_kind 2, _kernels_nb.py:288-337) and ``derivative`` (the non-local
-epilogue with the halo geometry, _kernels_nb.py:224-262; tap length 1 falls
-back to the plain engine plus a device-side global difference, ols.py).
-The host streaming and range paths take every kind but ``derivative``.
+epilogue with the halo geometry, _kernels_nb.py:224-262; tap length 1 runs
+through the range entries, whose geometry always has a halo).
+Every entry (device, host streaming, range, shard) takes every kind; the
+derivative's range geometry is t0 = M, L = N - M - 1 (olsb_input_extent_pp).
 """
 
 from __future__ import annotations

@@ -53,11 +53,15 @@ def shard_bounds(n_seg: int, valid_len: int, n_s: int, world: int) -> List[Tuple
     return out
 
 
-def make_shards(seg_plan: SegmentPlan, world: int,
-                extent=None) -> List[Shard]:
+def make_shards(seg_plan: SegmentPlan, world: int, extent=None,
+                postproc=None) -> List[Shard]:
     """Shard layout for every rank.  ``extent(g_lo, g_hi) -> (x_lo, x_hi)``
-    defaults to the engine's olsb_input_extent."""
-    extent = extent or (lambda a, b: input_extent(seg_plan, a, b))
+    defaults to the engine's input extent for post-process ``postproc``
+    (olsb_input_extent_pp: the derivative's halo geometry reads one more
+    segment of context than the plain one)."""
+    from .postproc import NONE
+    pp = postproc or NONE
+    extent = extent or (lambda a, b: input_extent(seg_plan, a, b, pp))
     n_s = seg_plan.signal_len
     shards = []
     for r, (g_lo, g_hi) in enumerate(shard_bounds(seg_plan.n_segments,

@@ -141,7 +141,8 @@ def test_autotune_segment_size(oc, mode):
 def test_sharded_outputs_bit_identical(oc, mode):
     # every rank's launch from its own halo'd input slice (make_shards +
     # convolve_shard, the multi-GPU data path without the transport) equals
-    # the single-call result bit for bit; r2r extents are pair-aligned
+    # the single-call result bit for bit; r2r extents are pair-aligned; the
+    # derivative's extents (make_shards(postproc=...)) carry its halo
     from paper_1910_01972_b200.sharding import convolve_shard, make_shards
     ns, m, nfil, n, origin = 20000, 400, 3, 2048, 17
     rng = np.random.default_rng([60, ns])
@@ -155,15 +156,17 @@ def test_sharded_outputs_bit_identical(oc, mode):
     fs = oc.transform_filters(oc.make_filterset(taps, origin, P), p,
                               "natural" if real else "permuted")
     sig = oc.make_signal(x, "real" if real else "complex", P)
-    full = oc.convolve(sig, fs, p)
-    for world in (2, 3, 5):
-        got = torch.full_like(full, float("nan"))
-        for sh in make_shards(p, world):
-            if sh.g_hi <= sh.g_lo:
-                continue
-            xl = sig.samples[sh.x_lo:sh.x_hi].clone()   # only this rank's data
-            got[:, sh.g_lo:sh.g_hi] = convolve_shard(xl, sh, p, fs)
-        assert torch.equal(got, full), world
+    for pp in (None, oc.PostProcSpec("derivative")):
+        full = oc.convolve(sig, fs, p, postproc=pp)
+        for world in (2, 3, 5):
+            got = torch.full_like(full, float("nan"))
+            for sh in make_shards(p, world, postproc=pp):
+                if sh.g_hi <= sh.g_lo:
+                    continue
+                xl = sig.samples[sh.x_lo:sh.x_hi].clone()   # this rank's data
+                got[:, sh.g_lo:sh.g_hi] = convolve_shard(xl, sh, p, fs,
+                                                         postproc=pp)
+            assert torch.equal(got, full), (world, pp)
 
 
 _VARIANT_SCRIPT = r"""
@@ -304,3 +307,54 @@ def test_r2r_spectra_from_engine_fft(oc):
         padded[:, :m] = taps
         want = np.fft.rfft(padded, axis=1)
         assert rel_l2_per_filter(fs.spectra.cpu().numpy(), want) <= 1e-6, n
+
+
+@pytest.mark.parametrize("mode", ["c2c", "r2r"])
+@pytest.mark.parametrize("m", [1, 65])
+def test_derivative_streaming_and_ranges(oc, mode, m):
+    """The derivative through the host streaming path (row chunks and segment
+    chunks) and the range entry: the halo geometry t0 = M, L = N - M - 1
+    (ols.py:137-146); for M = 1 too (where the reference recomputes seam
+    neighbours from the input).  Streaming is bit-identical to the device
+    path; all of it agrees with the float64 direct convolution's global
+    difference within the fp32 bar, and the Executor matches convolve()."""
+    from paper_1910_01972_b200.ols import fused_range_launch
+    ns, nfil, n, origin = 20001, 3, 256, (m // 2)
+    rng = np.random.default_rng([93, ns, m])
+    real = mode == "r2r"
+    x = rng.standard_normal(ns) if real else (rng.standard_normal(ns)
+                                              + 1j * rng.standard_normal(ns))
+    taps = rng.standard_normal((nfil, m)) if real else (
+        rng.standard_normal((nfil, m)) + 1j * rng.standard_normal((nfil, m)))
+    P = oc.Precision.single
+    vk = "real" if real else "complex"
+    p = oc.plan(ns, m, mode, origin, n)
+    pp = oc.PostProcSpec("derivative")
+    fs = oc.transform_filters(oc.make_filterset(taps, origin, P), p,
+                              "natural" if real else "permuted")
+    sig = oc.make_signal(x, vk, P)
+    dev = oc.convolve(sig, fs, p, postproc=pp)
+    # reference: global central difference of the float64 convolution
+    import oracle
+    y = oracle.direct_convolve(x, taps, origin)
+    y = y.real if real else y
+    d = np.empty_like(y)
+    d[:, 1:-1] = 0.5 * (y[:, 2:] - y[:, :-2])
+    d[:, 0] = y[:, 1] - y[:, 0]
+    d[:, -1] = y[:, -1] - y[:, -2]
+    assert rel_l2_per_filter(dev.cpu().numpy(), d) <= 2 * L2_TOL
+    hsig = oc.make_signal(torch.from_numpy(np.ascontiguousarray(x).astype(
+        np.float32 if real else np.complex64)).pin_memory(), vk, P, device="cpu")
+    for chunk in (None, 7):
+        host = torch.full(tuple(dev.shape), float("nan"),
+                          dtype=dev.dtype).pin_memory()
+        oc.convolve(hsig, fs, p, postproc=pp, out=host, chunk_segments=chunk)
+        assert torch.equal(host, dev.cpu()), chunk
+    # a range launch in the middle of the signal
+    lo, hi = 6000, 13001
+    out = torch.empty((nfil, hi - lo), dtype=dev.dtype, device="cuda")
+    fused_range_launch(sig.samples, 0, ns, fs.spectra_dev, nfil, p, lo, hi, pp,
+                       out, hi - lo, lo, P)
+    assert torch.equal(out, dev[:, lo:hi])
+    ex = oc.Executor(fs, p, pp)
+    assert torch.equal(ex(sig), dev)

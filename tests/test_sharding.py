@@ -49,6 +49,14 @@ def test_shards_partition_and_cover_dependencies(mode):
                     assert s.x_lo <= need_lo and s.x_hi >= need_hi
                     assert s.left_halo >= 0 and s.right_halo >= 0
             assert np.all(cov == 1), (ns, m, world)
+            # the derivative's shards also cover the neighbours' inputs
+            if n - m - 1 >= 1:
+                for s in make_shards(p, world,
+                                     postproc=oc.PostProcSpec("derivative")):
+                    if s.g_hi > s.g_lo:
+                        need_lo = max(0, s.g_lo - 1 - (m - 1) + origin)
+                        need_hi = min(ns, s.g_hi + 1 + origin)
+                        assert s.x_lo <= need_lo and s.x_hi >= need_hi
 
 
 def _worker(rank, world, port, case, ret):
