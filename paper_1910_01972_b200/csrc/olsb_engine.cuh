@@ -54,6 +54,9 @@ enum HMode : int {
   H_LDG = 0,  // read through L1 with __ldg at the multiply (fp64 policy)
   H_TEX = 3,  // texture fetches: the TEX data path runs beside the LSU pipe
               // that carries the shared-memory exchanges (fp32 policies)
+  H_TMA = 4,  // a CTA-shared two-slot ring in shared memory, filled by one
+              // TMA bulk copy per filter one filter ahead (full / empty
+              // mbarriers); no prefetch registers
 };
 
 // Kernel configuration.  SEGS segment groups per CTA, NBUF exchange buffers
@@ -98,6 +101,8 @@ struct KCfg {
   // H_TEX only: the next filter's spectrum is fetched into registers while
   // the current one is transformed (hides the L2 latency of the fetch)
   static constexpr bool PREF = PREF_ && HM_ == H_TEX && !dbl;
+  // H_TMA: spectrum ring in shared memory (fp32)
+  static constexpr bool HT = HM_ == H_TMA && !dbl;
   // ablation switches for bottleneck analysis (results are wrong with any
   // bit set): 1 no output stores, 2 no shared-memory traffic in the inverse
   // exchanges, 4 no inverse exchange barriers, 8 spectra of filters f & 1
@@ -133,7 +138,11 @@ struct KCfg {
   // [TMEM base address slot | MB: one mbarrier per segment group]
   static constexpr size_t f_mbar_off = f_slot_off + 16;
   static constexpr size_t f_jt_off = al(f_mbar_off + (MB ? 8 * SEGS : 0));
-  static constexpr size_t f_smem_bytes = f_jt_off + jt_bytes;
+  // HT: [two spectrum slots | full[2], empty[2] mbarriers]
+  static constexpr size_t h_slot_bytes = al(size_t(VPT) * T * 16);
+  static constexpr size_t f_ring_off = al(f_jt_off + jt_bytes);
+  static constexpr size_t f_hbar_off = f_ring_off + (HT ? 2 * h_slot_bytes : 0);
+  static constexpr size_t f_smem_bytes = f_hbar_off + (HT ? 32 : 0);
 };
 
 // configuration of the row kernels (filter spectra, standalone transforms)
@@ -178,6 +187,20 @@ __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
         : "r"(a), "r"(parity)
         : "memory");
   } while (!done);
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a),
+               "r"(bytes)
+               : "memory");
+}
+// one-dimensional TMA bulk copy global -> shared, completion on `mbar`
+__device__ __forceinline__ void tma_load_1d(uint32_t dst, const void* src,
+                                            uint32_t bytes, uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(mbar)
+      : "memory");
 }
 template <class C>
 __device__ __forceinline__ uint32_t group_mbar(int sl) {
@@ -818,6 +841,21 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
       item(blockIdx.x, g_, f0, w_);
     }
     fetch(f0);
+    if constexpr (C::HT) {
+      if (tid == 0) {
+        const uint32_t hb0 = uint32_t(__cvta_generic_to_shared(smem_raw + C::f_hbar_off));
+        mbar_init(hb0, 1);
+        mbar_init(hb0 + 8, 1);
+        mbar_init(hb0 + 16, C::THREADS / 32);
+        mbar_init(hb0 + 24, C::THREADS / 32);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        constexpr uint32_t hbytes = uint32_t(C::VPT) * C::T * 16;
+        mbar_expect_tx(hb0, hbytes);
+        tma_load_1d(uint32_t(__cvta_generic_to_shared(smem_raw + C::f_ring_off)),
+                    a.spec + size_t(f0) * (C::VPT * T), hbytes, hb0);
+      }
+    }
   }
 
   if constexpr (C::TMX) {
@@ -877,6 +915,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
 
   const R inv_n = R(1) / R(G::N);
   int xc = 0;
+  int hc = 0;  // HT: spectra consumed so far (ring slot hc & 1)
 
   for (long long it = blockIdx.x; it < nitems; it += gridDim.x) {
     long long grp = it / nfch;
@@ -997,6 +1036,31 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
           mulh(u, hn[u]);
         });
         if (f_next >= 0) fetch(f_next);
+      } else if constexpr (C::HT) {
+        const uint32_t hb0 = uint32_t(__cvta_generic_to_shared(smem_raw + C::f_hbar_off));
+        constexpr uint32_t hbytes = uint32_t(C::VPT) * C::T * 16;
+        if (tid == 0 && f_next >= 0) {
+          // the next spectrum into the other slot, once every warp has
+          // released that slot's previous contents (consumption hc - 1)
+          const int sn = (hc + 1) & 1;
+          if (hc >= 1) mbar_wait(hb0 + 16 + 8 * sn, uint32_t((hc - 1) >> 1) & 1u);
+          mbar_expect_tx(hb0 + 8 * sn, hbytes);
+          tma_load_1d(uint32_t(__cvta_generic_to_shared(smem_raw + C::f_ring_off)) +
+                          uint32_t(sn) * uint32_t(C::h_slot_bytes),
+                      a.spec + size_t(f_next) * (C::VPT * T), hbytes,
+                      hb0 + 8 * sn);
+        }
+        const int sc = hc & 1;
+        mbar_wait(hb0 + 8 * sc, uint32_t(hc >> 1) & 1u);
+        const float4* hs = reinterpret_cast<const float4*>(
+            smem_raw + C::f_ring_off + size_t(sc) * C::h_slot_bytes);
+        sfor<0, C::VPT>([&](auto uc) {
+          constexpr int u = decltype(uc)::value;
+          mulh(u, hs[spec_vec<R, LOGN>(t, u)]);
+        });
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(hb0 + 16 + 8 * sc);
+        ++hc;
       } else if constexpr (C::HM == H_TEX) {
         const int hb = a.hoff + f * (C::VPT * T);
         sfor<0, C::VPT>([&](auto uc) {

@@ -140,6 +140,29 @@ inline bool tail_forced() {
   return v;
 }
 
+// experiment: filter spectra through the shared-memory TMA ring (H_TMA)
+// instead of the TEX path (1: with the default TMEM residency, 2: TMX = 1)
+inline int htma_env() {
+  static int v = [] {
+    const char* e = getenv("OLSB_HTMA");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+template <class R, int LOGN, int TMX>
+using HtmaPolicy =
+    KCfg<R, LOGN, DefaultPolicy<R, LOGN>::SEGS, 1, H_TMA, 1,
+         DefaultPolicy<R, LOGN>::type::MINB, TMX, 0>;
+
+// experiment: cap on CTAs per SM of the fused launch (0 = the policy's)
+inline int grid_cap_env() {
+  static int v = [] {
+    const char* e = getenv("OLSB_GRID_CAP");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 inline int variant_env() {
   static int v = [] {
     const char* e = getenv("OLSB_VARIANT");
@@ -173,6 +196,8 @@ int launch_fused_cfg(FusedArgs<typename C::R> a, cudaStream_t st) {
   // the occupancy API reports one CTA per SM for kernels that allocate
   // tensor memory; the TMEM policies size their columns for MINB CTAs/SM
   if constexpr (C::TMX) resident = std::max(resident, C::MINB * num_sms());
+  if (grid_cap_env() > 0)
+    resident = std::min(resident, grid_cap_env() * num_sms());
   if constexpr (C::HM == H_TEX) {
     rc = bind_spectra(a, size_t(a.n_fil) * C::VPT * C::T * 16);
     if (rc) return rc;
@@ -374,6 +399,24 @@ int launch_fused(FusedArgs<R> a, int mode, cudaStream_t st) {
     }
   }
   if constexpr (std::is_same<R, float>::value) {
+    if (!a.xtw && variant_env() < 0 && htma_env()) {
+      if (a.n_fil == 1 || htma_env() == 3) {
+        using S = HtmaPolicy<R, LOGN, 0>;
+        if (mode == FMODE_R2R) return launch_fused_cfg<S, FMODE_R2R>(a, st);
+        if (mode == FMODE_ABS2) return launch_fused_cfg<S, FMODE_ABS2>(a, st);
+        return launch_fused_cfg<S>(a, st);
+      }
+      if (htma_env() == 2) {
+        using S = HtmaPolicy<R, LOGN, 1>;
+        if (mode == FMODE_R2R) return launch_fused_cfg<S, FMODE_R2R>(a, st);
+        if (mode == FMODE_ABS2) return launch_fused_cfg<S, FMODE_ABS2>(a, st);
+        return launch_fused_cfg<S>(a, st);
+      }
+      using S = HtmaPolicy<R, LOGN, 2>;
+      if (mode == FMODE_R2R) return launch_fused_cfg<S, FMODE_R2R>(a, st);
+      if (mode == FMODE_ABS2) return launch_fused_cfg<S, FMODE_ABS2>(a, st);
+      return launch_fused_cfg<S>(a, st);
+    }
     if (a.n_fil == 1 && !a.xtw && variant_env() < 0) {
       using S = SingleFilterPolicy<R, LOGN>;
       if (mode == FMODE_R2R) return launch_fused_cfg<S, FMODE_R2R>(a, st);

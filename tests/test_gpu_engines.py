@@ -60,3 +60,23 @@ def test_experimental_engine_parity(env, n):
     assert res.returncode == 0, res.stdout + res.stderr
     worst = float(res.stdout.split("WORST")[-1])
     assert worst <= 1e-5, (env, worst)
+
+
+@pytest.mark.parametrize("val", ["1", "2", "3"])
+def test_tma_spectrum_ring_parity(val):
+    """OLSB_HTMA: filter spectra through the shared-memory TMA ring (full /
+    empty mbarriers, one filter ahead) -- 1: TMEM residency, 2: TMX = 1,
+    3: register policy; F = 1 cells take the register policy.  Filter counts
+    1-5 exercise the ring's slot and phase turnover across items."""
+    cells = []
+    for n in (64, 256, 1024, 2048, 4096):
+        m = n // 4 + 1
+        cells += [(3 * n + 5, m, 1, n, 0), (20 * n + 11, m, 5, n, m // 3),
+                  (9 * n + 3, m, 2, n, 1)]
+    code = SCRIPT % {"root": ROOT, "cells": cells}
+    res = subprocess.run([sys.executable, "-c", code], capture_output=True,
+                         text=True, env=dict(os.environ, OLSB_HTMA=val),
+                         timeout=600)
+    assert res.returncode == 0, res.stdout + res.stderr
+    worst = float(res.stdout.split("WORST")[-1])
+    assert worst <= 1e-5, (val, worst)
