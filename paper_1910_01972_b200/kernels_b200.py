@@ -175,13 +175,17 @@ def fused_c2c(x, spectra, tw, twc, m, origin, l_eff, t0, win_off,
     n_s, n = x.shape[0], spectra.shape[1]
     if seg_hi <= seg_lo or spectra.shape[0] == 0:
         return
-    if pp_kind == PP_DERIV and m == 1:
-        # tap length 1 has no halo: the reference recomputes the seam
-        # neighbours from the input (_store, :232-260); y = h0 x exactly
-        _deriv_single_tap(x, h0, origin, l_eff, seg_lo, seg_hi, out)
-        return
     sd = _engine_spectra(spectra, n)
     xd, od, g_lo, g_hi = _window_io(x, out, l_eff, seg_lo, seg_hi)
+    if pp_kind == PP_DERIV and m == 1:
+        # tap length 1 leaves no aliased sample for a halo in the reference's
+        # geometry (it recomputes the seam neighbours from the input, _store
+        # :232-260); the range entry's derivative geometry (t0 = 1, L = N -
+        # 2) keeps both neighbours inside every segment
+        _range_deriv("olsb_fused_c2c_range", xd, sd, spectra.shape[0], n, m,
+                     origin, pp_c, od, g_lo, g_hi, x)
+        _write_back(out, od, g_lo, g_hi)
+        return
     common = (xd.data_ptr(), 0, n_s, sd.data_ptr(), spectra.shape[0], n, m,
               origin, l_eff, t0, win_off, seg_lo, seg_hi, int(pp_kind),
               float(pp_c))
@@ -226,9 +230,6 @@ def fused_r2r(x, spectra, tw_half, tw_half_conj, pack_tw, pack_tw_conj,
     n = 2 * h
     if seg_hi <= seg_lo or spectra.shape[0] == 0:
         return
-    if pp_kind == PP_DERIV and m == 1:
-        _deriv_single_tap(x, h0, origin, l_eff, seg_lo, seg_hi, out)
-        return
     cdt = np.complex64 if x.dtype == np.float32 else np.complex128
     full = np.empty((spectra.shape[0], n), dtype=cdt)
     full[:, :h + 1] = spectra
@@ -239,6 +240,11 @@ def fused_r2r(x, spectra, tw_half, tw_half_conj, pack_tw, pack_tw_conj,
     sd = _engine_spectra(perm, n, key_extra=("r2r",
                                              spectra.__array_interface__["data"][0]))
     xd, od, g_lo, g_hi = _window_io(x, out, l_eff, seg_lo, seg_hi)
+    if pp_kind == PP_DERIV and m == 1:     # as fused_c2c
+        _range_deriv("olsb_fused_r2r_range", xd, sd, spectra.shape[0], n, m,
+                     origin, pp_c, od, g_lo, g_hi, x)
+        _write_back(out, od, g_lo, g_hi)
+        return
     _lib.call("olsb_fused_r2r", xd.data_ptr(), 0, n_s, sd.data_ptr(),
               spectra.shape[0], n, m, origin, l_eff, t0, win_off, seg_lo,
               seg_hi, int(pp_kind), float(pp_c), od.data_ptr(), od.shape[1],
@@ -246,28 +252,11 @@ def fused_r2r(x, spectra, tw_half, tw_half_conj, pack_tw, pack_tw_conj,
     _write_back(out, od, g_lo, g_hi)
 
 
-def _deriv_single_tap(x, h0, origin, l_eff, seg_lo, seg_hi, out):
-    """Derivative post-process for tap length 1 (y = h0[f] x[g + origin],
-    origin = 0 for M = 1): central difference, one-sided at the signal ends
-    (_store kind 3, _kernels_nb.py:226-262), on the device."""
-    n_s = x.shape[0]
-    g_lo, g_hi = seg_lo * l_eff, min(seg_hi * l_eff, n_s)
+def _range_deriv(entry, xd, sd, n_fil, n, m, origin, pp_c, od, g_lo, g_hi, x):
+    """Outputs [g_lo, g_hi) with the derivative epilogue through the range
+    entry (olsb_fused_{c2c,r2r}_range, halo geometry) into the tile ``od``."""
     if g_hi <= g_lo:
         return
-    xd = _to_dev(x)
-    hd = _to_dev(np.asarray(h0))
-    gl = max(0, g_lo - 1)
-    gr = min(n_s, g_hi + 1)
-    y = hd[:, None] * xd[None, gl:gr]
-    d = torch.empty((y.shape[0], g_hi - g_lo), dtype=y.dtype, device=y.device)
-    idx = torch.arange(g_lo, g_hi, device=y.device) - gl
-    left = torch.clamp(idx - 1, min=0)
-    right = torch.clamp(idx + 1, max=y.shape[1] - 1)
-    d[:] = 0.5 * (y[:, right] - y[:, left])
-    if g_lo == 0 and n_s > 1:
-        d[:, 0] = y[:, 1 - gl] - y[:, 0 - gl]
-    if g_hi == n_s and n_s > 1:
-        d[:, -1] = y[:, n_s - 1 - gl] - y[:, n_s - 2 - gl]
-    if n_s == 1:
-        d.zero_()
-    out[:, g_lo:g_hi] = d.cpu().numpy().astype(out.dtype, copy=False)
+    _lib.call(entry, xd.data_ptr(), 0, x.shape[0], sd.data_ptr(), n_fil, n, m,
+              origin, g_lo, g_hi, PP_DERIV, float(pp_c), od.data_ptr(),
+              od.shape[1], g_lo, _prec(x), _stream())

@@ -151,3 +151,61 @@ def test_fused_r2r_reference_contract():
         assert np.all(np.isnan(out[:, g_hi:]))
     ref = oracle.direct_convolve(x, taps, origin).real
     assert rel_l2_per_filter(out, ref) <= 1e-5
+
+
+def _global_derivative(y):
+    """_store kind 3's global rule: central difference, one-sided at the
+    signal ends (_kernels_nb.py:224-262)"""
+    d = np.empty_like(y)
+    d[:, 1:-1] = 0.5 * (y[:, 2:] - y[:, :-2])
+    d[:, 0] = y[:, 1] - y[:, 0]
+    d[:, -1] = y[:, -1] - y[:, -2]
+    return d
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m", [1, 129])
+def test_fused_derivative_reference_contract(m):
+    """K.fused_c2c / K.fused_r2r with pp_kind 3 (derivative) over uneven
+    worker ranges, called with the reference's own derivative geometry
+    (output_windows with halo 1: l_eff = N - M - 1 for M > 1, N - M + 1 with
+    t0 = M - 1 for M = 1, ols.py:137-146): only the range's windows are
+    written, and the result matches the float64 global derivative."""
+    assert has_gpu()
+    from paper_1910_01972_b200 import kernels_b200 as K
+    n, ns, origin = 512, 9001, m // 2
+    rng = np.random.default_rng([98, m])
+    halo = 1 if m > 1 else 0
+    l_eff = n - m + 1 - 2 * halo
+    t0 = m - 1 + halo
+    win_off = origin - (m - 1) - halo
+    n_seg = -(-ns // l_eff)
+    for real in (False, True):
+        if real:
+            x = rng.standard_normal(ns).astype(np.float32)
+            taps = rng.standard_normal((3, m))
+            padded = np.zeros((3, n))
+            padded[:, :m] = taps
+            spec = np.fft.rfft(padded, axis=1).astype(np.complex64)
+            out = np.full((3, ns), np.nan, np.float32)
+        else:
+            x = (rng.standard_normal(ns) + 1j * rng.standard_normal(ns)).astype(np.complex64)
+            taps = rng.standard_normal((3, m)) + 1j * rng.standard_normal((3, m))
+            spec = np.asarray(oracle.transform_filters(taps, n, "single"),
+                              dtype=np.complex64)
+            out = np.full((3, ns), np.nan, np.complex64)
+        h0 = taps[:, 0]
+        for lo, hi in _splits(n_seg):
+            if real:
+                K.fused_r2r(x, spec, None, None, None, None, m, origin, l_eff,
+                            t0, win_off, lo, hi, 3, 1.0, h0, out, None, None,
+                            None, None)
+            else:
+                K.fused_c2c(x, spec, None, None, m, origin, l_eff, t0, win_off,
+                            lo, hi, 3, 1.0, h0, out, None, None)
+            g_hi = min(hi * l_eff, ns)
+            assert np.all(np.isfinite(out[:, :g_hi]))
+            assert np.all(np.isnan(out[:, g_hi:]))
+        y = oracle.direct_convolve(x, taps, origin)
+        ref = _global_derivative(y.real if real else y)
+        assert rel_l2_per_filter(out, ref) <= 2e-5, (m, real)
