@@ -221,6 +221,21 @@ def transform_filters(filters: FilterSet, seg_plan: SegmentPlan,
                       spectra.data_ptr(), dev.data_ptr(), precision.code,
                       _stream_ptr())
         return filters.with_spectra(spectra, layout, n, dev)
+    if n <= 4096:
+        # natural order (the comparison variants' layout): the engine's own
+        # in-register FFT, read out of the permuted spectrum (bin k at
+        # bit-reversed position rev(k)), as for the real path
+        perm = torch.empty((filters.n_filters, n), dtype=precision.torch_complex,
+                           device=taps.device)
+        dev = torch.empty_like(perm)
+        with torch.cuda.device(taps.device):
+            _lib.call("olsb_filter_spectra_c2c", ctaps.data_ptr(),
+                      filters.n_filters, filters.tap_length, n,
+                      perm.data_ptr(), dev.data_ptr(), precision.code,
+                      _stream_ptr())
+        nat = perm[:, _bitrev_index(n, taps.device)].contiguous()
+        return filters.with_spectra(nat, layout, n)
+    # segment lengths beyond the engine's (comparison paths only): cuFFT
     padded = torch.zeros((filters.n_filters, n), dtype=precision.torch_complex,
                          device=taps.device)
     padded[:, :filters.tap_length] = ctaps

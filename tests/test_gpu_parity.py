@@ -118,6 +118,24 @@ def test_transform_filters_known_answers(oc):
         assert np.allclose(c.spectra[0].cpu(), np.ones(8))
 
 
+def test_natural_spectra_from_engine_fft(oc):
+    # "natural" c2c spectra (the comparison variants' layout) come from the
+    # engine's in-register FFT read out in natural order: numpy's fft of the
+    # zero-padded taps within the fp32 / fp64 transform error
+    rng = np.random.default_rng(31)
+    for prec, tol in (("single", 2e-6), ("double", 1e-13)):
+        P = oc.Precision(prec)
+        for n, m in ((4, 3), (64, 17), (1024, 257), (4096, 1000)):
+            taps = rng.standard_normal((3, m)) + 1j * rng.standard_normal((3, m))
+            fs = oc.transform_filters(oc.make_filterset(taps, 0, P),
+                                      oc.plan(5 * n, m, "c2c", 0, n), "natural")
+            padded = np.zeros((3, n), np.complex128)
+            padded[:, :m] = taps
+            want = np.fft.fft(padded, axis=1)
+            got = fs.spectra.cpu().numpy()
+            assert np.linalg.norm(got - want) / np.linalg.norm(want) <= tol, (prec, n)
+
+
 # ---------------------------------------------------------------------------
 # fused engine vs the reference (golden grid incl. edge cases)
 # ---------------------------------------------------------------------------
