@@ -594,11 +594,68 @@ __device__ __forceinline__ int top_bits(int t) {
 }
 
 
+// Warp bits (thread bits 5 .. LOGT-1) that map to the same index bit in
+// windows X and X+1: the exchange between them only couples the warps that
+// agree on those bits (each such warp subset reads back only what it wrote).
+template <class G, int X>
+constexpr int common_warp_bits() {
+  int m = 0;
+  for (int b = 5; b < G::LOGT; ++b)
+    if (G::thread_part(X, 1 << b) == G::thread_part(X + 1, 1 << b)) m |= 1 << b;
+  return m;
+}
+template <class G, int X>
+constexpr bool split_exchange() {
+  constexpr int m = common_warp_bits<G, X>();
+  return m != 0 && (m & (m - 1)) == 0;  // exactly one common warp bit
+}
+template <class G, int X>
+constexpr int split_bit() {
+  constexpr int m = common_warp_bits<G, X>();
+  int b = 0;
+  while (b < 31 && !((m >> b) & 1)) ++b;
+  return b;
+}
+
 // exchange: write window QW, barrier, read window QR (ABL: ablation bits)
+//
+// NBUF = 3 (one segment per CTA): the inverse exchanges whose windows share
+// one warp bit (split_exchange: N = 4096's first inverse exchange couples 4
+// of the segment's 8 warps) use buffer 0 and a barrier over those warps
+// only; the other inverse exchanges alternate buffers 1 and 2 with one full
+// barrier each (the buffer they overwrite was last read before the previous
+// full barrier).  Forward exchanges (once per item) fence both sides with
+// full barriers, so the inverse never races with them.
 template <class C, int QW, int QR, int ABL = 0>
 __device__ __forceinline__ void exchange(Cpx<typename C::R>* bufs, int& xc,
                                          int sl, int t, Cpx<typename C::R>* x,
                                          IC<ABL> = {}) {
+  if constexpr (C::NBUF == 3) {
+    static_assert(C::SEGS == 1, "NBUF = 3 takes one segment per CTA");
+    constexpr int X3 = QW < QR ? QW : QR;
+    Cpx<typename C::R>* b3 = bufs;
+    if constexpr (QW > QR) {  // forward
+      b3 += (X3 & 1) * C::buf_elems;
+      __syncthreads();
+      smem_store<C, QW, X3>(b3, t, x);
+      __syncthreads();
+      smem_load<C, QR, X3>(b3, t, x);
+      __syncthreads();
+    } else if constexpr (split_exchange<typename C::G, X3>()) {
+      constexpr int sb = split_bit<typename C::G, X3>();
+      smem_store<C, QW, X3>(b3, t, x);
+      asm volatile("bar.sync %0, %1;" ::"r"(2 + ((t >> sb) & 1)), "r"(C::T / 2)
+                   : "memory");
+      smem_load<C, QR, X3>(b3, t, x);
+    } else {
+      b3 += (1 + ((xc >> 1) & 1)) * C::buf_elems;
+      smem_store<C, QW, X3>(b3, t, x);
+      __syncthreads();
+      smem_load<C, QR, X3>(b3, t, x);
+    }
+    ++xc;
+    return;
+  }
   Cpx<typename C::R>* buf = bufs + (C::NBUF == 2 ? (xc & 1) * C::buf_elems : 0) +
                             size_t(sl) * C::L::stride;
   constexpr int X = QW < QR ? QW : QR;  // exchange between windows X, X+1

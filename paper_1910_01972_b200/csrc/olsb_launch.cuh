@@ -376,10 +376,26 @@ int launch_w32x2(FusedArgs<float> a, cudaStream_t st) {
   return int(cudaGetLastError());
 }
 
+// N = 4096 with split coupling (NBUF = 3, olsb_engine.cuh exchange()):
+// selected with OLSB_N3=1
+inline int n3_env() {
+  static int v = [] {
+    const char* e = getenv("OLSB_N3");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 template <class R, int LOGN>
 int launch_fused(FusedArgs<R> a, int mode, cudaStream_t st) {
   using D = typename DefaultPolicy<R, LOGN>::type;
   if constexpr (std::is_same<R, float>::value && LOGN == 12) {
+    if (!a.xtw && variant_env() < 0 && n3_env() &&
+        (a.pp_kind == OLSB_PP_NONE || a.pp_kind == OLSB_PP_SCALE)) {
+      using S = KCfg<float, 12, 1, 3, H_TEX, 1, 2, 2, 1>;
+      if (mode == FMODE_C2C) return launch_fused_cfg<S, FMODE_C2C>(a, st);
+      if (mode == FMODE_ABS2) return launch_fused_cfg<S, FMODE_ABS2>(a, st);
+    }
     if (!a.xtw && variant_env() < 0 && w64x2_env() &&
         (a.pp_kind == OLSB_PP_NONE || a.pp_kind == OLSB_PP_SCALE)) {
       if (mode == FMODE_C2C) return launch_w64x2<FMODE_C2C>(a, st);
