@@ -594,68 +594,18 @@ __device__ __forceinline__ int top_bits(int t) {
 }
 
 
-// Warp bits (thread bits 5 .. LOGT-1) that map to the same index bit in
-// windows X and X+1: the exchange between them only couples the warps that
-// agree on those bits (each such warp subset reads back only what it wrote).
-template <class G, int X>
-constexpr int common_warp_bits() {
-  int m = 0;
-  for (int b = 5; b < G::LOGT; ++b)
-    if (G::thread_part(X, 1 << b) == G::thread_part(X + 1, 1 << b)) m |= 1 << b;
-  return m;
+// some exchange of the transform is warp-local (Geo::warp_local)
+template <class G>
+constexpr bool any_warp_local() {
+  bool r = false;
+  for (int x = 0; x + 1 < G::P; ++x) r = r || G::warp_local(x);
+  return r;
 }
-template <class G, int X>
-constexpr bool split_exchange() {
-  constexpr int m = common_warp_bits<G, X>();
-  return m != 0 && (m & (m - 1)) == 0;  // exactly one common warp bit
-}
-template <class G, int X>
-constexpr int split_bit() {
-  constexpr int m = common_warp_bits<G, X>();
-  int b = 0;
-  while (b < 31 && !((m >> b) & 1)) ++b;
-  return b;
-}
-
 // exchange: write window QW, barrier, read window QR (ABL: ablation bits)
-//
-// NBUF = 3 (one segment per CTA): the inverse exchanges whose windows share
-// one warp bit (split_exchange: N = 4096's first inverse exchange couples 4
-// of the segment's 8 warps) use buffer 0 and a barrier over those warps
-// only; the other inverse exchanges alternate buffers 1 and 2 with one full
-// barrier each (the buffer they overwrite was last read before the previous
-// full barrier).  Forward exchanges (once per item) fence both sides with
-// full barriers, so the inverse never races with them.
 template <class C, int QW, int QR, int ABL = 0>
 __device__ __forceinline__ void exchange(Cpx<typename C::R>* bufs, int& xc,
                                          int sl, int t, Cpx<typename C::R>* x,
                                          IC<ABL> = {}) {
-  if constexpr (C::NBUF == 3) {
-    static_assert(C::SEGS == 1, "NBUF = 3 takes one segment per CTA");
-    constexpr int X3 = QW < QR ? QW : QR;
-    Cpx<typename C::R>* b3 = bufs;
-    if constexpr (QW > QR) {  // forward
-      b3 += (X3 & 1) * C::buf_elems;
-      __syncthreads();
-      smem_store<C, QW, X3>(b3, t, x);
-      __syncthreads();
-      smem_load<C, QR, X3>(b3, t, x);
-      __syncthreads();
-    } else if constexpr (split_exchange<typename C::G, X3>()) {
-      constexpr int sb = split_bit<typename C::G, X3>();
-      smem_store<C, QW, X3>(b3, t, x);
-      asm volatile("bar.sync %0, %1;" ::"r"(2 + ((t >> sb) & 1)), "r"(C::T / 2)
-                   : "memory");
-      smem_load<C, QR, X3>(b3, t, x);
-    } else {
-      b3 += (1 + ((xc >> 1) & 1)) * C::buf_elems;
-      smem_store<C, QW, X3>(b3, t, x);
-      __syncthreads();
-      smem_load<C, QR, X3>(b3, t, x);
-    }
-    ++xc;
-    return;
-  }
   Cpx<typename C::R>* buf = bufs + (C::NBUF == 2 ? (xc & 1) * C::buf_elems : 0) +
                             size_t(sl) * C::L::stride;
   constexpr int X = QW < QR ? QW : QR;  // exchange between windows X, X+1
@@ -667,7 +617,12 @@ __device__ __forceinline__ void exchange(Cpx<typename C::R>* bufs, int& xc,
   if constexpr (C::MB) {
     // the previous exchange's loads are done in every warp of the group
     if (xc > 0) mbar_wait(group_mbar<C>(sl), uint32_t(xc - 1) & 1u);
-  } else if constexpr (C::NBUF == 1 && !(ABL & 4)) {
+  } else if constexpr ((C::NBUF == 1 ||
+                        (!WL && any_warp_local<typename C::G>())) &&
+                       !(ABL & 4)) {
+    // NBUF = 2 skips this barrier because the previous exchange's barrier
+    // orders the loads of the one before it; a warp-local previous exchange
+    // (only __syncwarp) does not, so cross-warp exchanges then keep it
     group_sync<C>(sl);
   }
   if constexpr (!(ABL & 2)) smem_store<C, QW, X>(buf, t, x);
@@ -1224,7 +1179,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
               y[e] = Cpx<R>{dv(g, l.re, y[e].re, r.re),
                             dv(gi, l.im, y[e].im, r.im)};
             });
-            if constexpr (C::NBUF == 2 || C::MB) group_sync<C>(sl);  // next exchange
+            if constexpr (C::NBUF >= 2 || C::MB) group_sync<C>(sl);  // next exchange
           }
         }
       }

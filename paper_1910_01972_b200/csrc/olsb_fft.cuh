@@ -91,9 +91,14 @@ struct Geo {
   // With the plain mapping (thread bit i -> index bit i for i < lo) that
   // holds iff lo >= 7; a lower window with at least two warp bits to spare
   // swaps thread bits (lo-2, lo-1) with the top two thread bits instead.
+  // Not at N = 4096: there the plain mapping makes the first inverse
+  // exchange warp-local (warp bits = index bits 9-11 in both windows), which
+  // saves one of its two 8-warp barriers per filter and outweighs the plain
+  // (non-tangent) forms of window 1's first two stages (-4% on the cfg5
+  // shard); at N = 2048 the remap wins (+5% without it).
   static constexpr bool remap(int q) {
-    return OLSB_MID_REMAP && q >= 1 && lo(q) >= 2 && lo(q) < 7 && LOGT >= 7 &&
-           lo(q) <= LOGT - 2;
+    return OLSB_MID_REMAP && LOGN != 12 && q >= 1 && lo(q) >= 2 && lo(q) < 7 &&
+           LOGT >= 7 && lo(q) <= LOGT - 2;
   }
   // windows whose first two stages use the FMA (tangent) forms
   static constexpr bool tan01(int q) {
@@ -144,21 +149,25 @@ struct Pad {
 };
 
 constexpr Pad pad_for(bool dbl, int logn) {
-  // LOGN 11 / 12 carry the Geo::remap thread-bit swap of the middle window
+  // LOGN 11 carries the Geo::remap thread-bit swap of the middle window
   constexpr Pad f[13] = {{2, 0, 2, 0, 2, 0, 2},    {2, 0, 2, 0, 2, 0, 2},
                          {2, 0, 2, 0, 2, 0, 6},    {2, 0, 2, 0, 2, 0, 10},
                          {2, 0, 2, 0, 2, 0, 18},   {2, 0, 4, 8, 4, 0, 42},
                          {4, 2, 5, 4, 5, 0, 76},   {2, 0, 4, 2, 4, 0, 152},
                          {2, 0, 4, 2, 4, 0, 286},  {4, 2, 7, 2, 7, 0, 580},
                          {4, 2, 7, 4, 7, 0, 1178}, {4, 2, 7, 2, 10, 4, 2336},
-                         {4, 2, 10, 4, 10, 0, 4618}};
+                         {2, 0, 4, 2, 4, 0, 4606}};
   constexpr Pad d[13] = {{2, 0, 2, 0, 2, 0, 1},    {2, 0, 2, 0, 2, 0, 1},
                          {2, 0, 2, 0, 2, 0, 5},    {2, 0, 2, 0, 2, 0, 9},
                          {2, 0, 2, 0, 2, 0, 17},   {2, 0, 4, 1, 4, 0, 34},
                          {2, 0, 4, 1, 4, 0, 68},   {2, 0, 4, 1, 4, 0, 135},
                          {2, 0, 4, 1, 4, 0, 271},  {2, 0, 4, 1, 4, 0, 543},
                          {2, 0, 4, 1, 4, 0, 1087}, {4, 1, 9, 2, 9, 0, 2181},
-                         {4, 1, 10, 4, 10, 0, 4363}};
+                         {2, 0, 4, 1, 4, 0, 4351}};
+#if !OLSB_MID_REMAP
+  // A/B builds without the middle-window remap: the round-1 layouts
+  if (!dbl && logn == 11) return Pad{4, 2, 7, 8, 7, 0, 2422};
+#endif
   return dbl ? d[logn] : f[logn];
 }
 

@@ -83,7 +83,10 @@ struct DefaultPolicy {
   // fp32 (OLSB_VARIANT=2 / 3 of the sweep in DESIGN.md §5, plus BAR = 1): 128-thread CTAs,
   // 4 CTAs per SM, segment spectrum and runtime-window twiddles in TMEM, the
   // next filter's spectrum prefetched through the TEX path; N = 4096 double
-  // buffers the exchange (one barrier per exchange).
+  // buffers the exchanges: its first inverse exchange is warp-local (no
+  // Geo::remap at N = 4096, only __syncwarp), the second keeps a barrier on
+  // both sides (a third buffer would remove one, but the 113 KB of shared
+  // memory per CTA leave too little L1 for the spectrum fetches: slower).
   // fp64: 128-thread CTAs (256 for N = 4096) at 3 CTAs/SM, 170 registers
   // (OLSB_DVARIANT sweep: cfg3 shape 5.65 vs 6.12 ms for 256-thread CTAs at
   // one CTA/SM)
@@ -376,26 +379,10 @@ int launch_w32x2(FusedArgs<float> a, cudaStream_t st) {
   return int(cudaGetLastError());
 }
 
-// N = 4096 with split coupling (NBUF = 3, olsb_engine.cuh exchange()):
-// selected with OLSB_N3=1
-inline int n3_env() {
-  static int v = [] {
-    const char* e = getenv("OLSB_N3");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
-}
-
 template <class R, int LOGN>
 int launch_fused(FusedArgs<R> a, int mode, cudaStream_t st) {
   using D = typename DefaultPolicy<R, LOGN>::type;
   if constexpr (std::is_same<R, float>::value && LOGN == 12) {
-    if (!a.xtw && variant_env() < 0 && n3_env() &&
-        (a.pp_kind == OLSB_PP_NONE || a.pp_kind == OLSB_PP_SCALE)) {
-      using S = KCfg<float, 12, 1, 3, H_TEX, 1, 2, 2, 1>;
-      if (mode == FMODE_C2C) return launch_fused_cfg<S, FMODE_C2C>(a, st);
-      if (mode == FMODE_ABS2) return launch_fused_cfg<S, FMODE_ABS2>(a, st);
-    }
     if (!a.xtw && variant_env() < 0 && w64x2_env() &&
         (a.pp_kind == OLSB_PP_NONE || a.pp_kind == OLSB_PP_SCALE)) {
       if (mode == FMODE_C2C) return launch_w64x2<FMODE_C2C>(a, st);

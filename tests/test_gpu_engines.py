@@ -48,7 +48,7 @@ print("WORST", worst)
 
 
 @pytest.mark.parametrize("env,n", [("OLSB_W64", 2048), ("OLSB_W32X2", 2048),
-                                   ("OLSB_W64X2", 4096), ("OLSB_N3", 4096)])
+                                   ("OLSB_W64X2", 4096)])
 def test_experimental_engine_parity(env, n):
     m = n // 4 + 17
     cells = [(3 * n + 5, m, 3, n, 0), (20 * n + 11, m, 5, n, m // 3),

@@ -7,7 +7,7 @@ L=gpurun_out/sanitize.log
 CS=/usr/local/cuda/bin/compute-sanitizer
 echo "## plain run" >> $L
 timeout 600 python tools/sanitize_cells.py >> $L 2>&1 || echo "plain rc=$?" >> $L
-for env in "" "OLSB_W64=1" "OLSB_W64X2=1" "OLSB_W32X2=1" "OLSB_N3=1" "OLSB_HTMA=1" "OLSB_HTMA=3"; do
+for env in "" "OLSB_W64=1" "OLSB_W64X2=1" "OLSB_W32X2=1" "OLSB_HTMA=1" "OLSB_HTMA=3"; do
   for tool in memcheck racecheck; do
     echo "## $tool ${env:-default}" >> $L
     env $env timeout 1500 $CS --tool $tool --print-limit 20 python tools/sanitize_cells.py 2>&1 \

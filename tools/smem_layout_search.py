@@ -34,8 +34,8 @@ def perm(logn, q, t):
     with the top two thread bits so the tangent-form choice is warp-uniform."""
     loge, logt, p, g0, los = geo(logn)
     lo = los[q]
-    if not (q >= 1 and 2 <= lo < 7 and logt >= 7 and lo <= logt - 2):
-        return t
+    if logn == 12 or not (q >= 1 and 2 <= lo < 7 and logt >= 7 and lo <= logt - 2):
+        return t     # (not at LOGN = 12: see Geo::remap)
     a, b = lo - 2, logt - 2
     x = ((t >> a) ^ (t >> b)) & 3
     return t ^ (x << a) ^ (x << b)
